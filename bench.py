@@ -1,0 +1,478 @@
+#!/usr/bin/env python
+"""Benchmark: batched fused negacyclic polymul, BASELINE cfg3
+(N = 2^16, 21 x 60-bit RNS limbs), on N GPUs (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = one fused polymul of every (ciphertext, limb) pair of a
+[batch, 21, 65536] residue batch (batch ciphertexts per GPU, weak scaling:
+shards are independent ciphertexts, no collective on the data path).  The
+timed region is K steps on the device (CUDA events on the launch stream,
+barrier + synchronize on both sides, max over ranks).  Inputs (2 x 176 MiB at
+batch 16) exceed the 126 MB L2, so no flush is needed between steps.
+
+Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "polymuls/sec at N=2^16×21 limbs; NTT µs; % of HBM/int-pipe roofline"
+UNIT = "ct-polymul/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--batch", type=int, default=16, help="ciphertexts per GPU")
+    ap.add_argument("--log-n", type=int, default=16)
+    ap.add_argument("--limbs", type=int, default=21)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU work for the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (nvidia-smi, B200_PROFILING.md)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001 - sampling is best-effort
+                return
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()),
+                 default=None)
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7])
+                          if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+def make_inputs(primes, batch: int, n: int, seed: int):
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    out = np.empty((batch, len(primes), n), dtype=np.uint64)
+    for li, q in enumerate(primes):
+        out[:, li, :] = rng.integers(0, q, size=(batch, n), dtype=np.uint64)
+    return out
+
+
+def modmuls_per_product(n: int) -> int:
+    """Reference OpCounter modmul count of one polymul_fused."""
+    lg = n.bit_length() - 1
+    return (3 * n // 2) * (lg - 1) + 2 * n
+
+
+def row_kernel_modmuls(n: int) -> int:
+    """Algorithmic modmuls done inside the fused ROW kernel per product:
+    forward row stages of a and b (log2 N2 - 1 each, n/2 per stage), the
+    fused middle (4 per pair = 2n) and the inverse row stages."""
+    n2 = min(n, 4096)
+    l2 = n2.bit_length() - 1
+    return 2 * (n // 2) * (l2 - 1) + 2 * n + (n // 2) * (l2 - 1)
+
+
+def cpu_reference_rate(basis_primes, psis, n, A, B, seconds: float, threads: int):
+    """Reference CPU polymul_fused (oracle/_ref, native Cython, GIL released)
+    over a bounded sample; returns (ct/s, kind, cores, sample, outputs)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+
+    nt = oracle.reference()
+    L = len(basis_primes)
+    if nt is not None:
+        kind = "reference"
+        fplans = []
+        for q, psi in zip(basis_primes, psis):
+            plan = nt.params._plan_from_root(n, n.bit_length() - 1, nt.Modulus(q), psi,
+                                             "proposed")
+            fplans.append(nt.FusedPlan.from_plan(plan))
+
+        def one(bi, li):
+            return nt.polymul_fused(nt.Polynomial(A[bi, li]), nt.Polynomial(B[bi, li]),
+                                    fplans[li])
+    else:
+        kind = "port"
+        tables = [oracle.twiddles(q, psi, n.bit_length() - 1)
+                  for q, psi in zip(basis_primes, psis)]
+
+        def one(bi, li):
+            return oracle.polymul_fused(A[bi, li], B[bi, li], basis_primes[li], 0,
+                                        tables=tables[li])
+
+    def run(nct):
+        items = [(bi % A.shape[0], li) for bi in range(nct) for li in range(L)]
+        step = -(-len(items) // threads)
+        spans = [items[i:i + step] for i in range(0, len(items), step)]
+        outs = {}
+
+        def span(sp):
+            for bi, li in sp:
+                outs[(bi, li)] = one(bi, li)
+
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            list(pool.map(span, spans))
+        return time.perf_counter() - t0, outs
+
+    dt1, outs = run(1)
+    nct = max(1, int(seconds / max(dt1, 1e-3)))
+    dt, _ = run(nct)
+    rate = nct / dt
+    sample = (f"{nct} ciphertext(s) x {L} limbs of N={n} via "
+              f"{'nttmul.polymul_fused(Polynomial, Polynomial, FusedPlan)' if kind == 'reference' else 'oracle C port'}"
+              f", {threads} threads, {dt:.2f} s")
+    first = np.stack([outs[(0, li)] for li in range(L)])
+    return rate, kind, threads, sample, first
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import numpy as np
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2209_01290_b200 as nt
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, L, Bn = 1 << args.log_n, args.limbs, args.batch
+    basis = nt.RnsBasis.build(n, 60, L, seed=0)
+    primes = list(basis.primes)
+    psis = [p.psi for p in basis.plans]
+    A_h = make_inputs(primes, Bn, n, seed=1000 + rank)
+    B_h = make_inputs(primes, Bn, n, seed=2000 + rank)
+    A = torch.from_numpy(A_h).cuda()
+    B = torch.from_numpy(B_h).cuda()
+    C = torch.empty_like(A)
+    W = torch.empty_like(A)
+    fwd, inv, limbs = basis.device_tables()
+    stream = torch.cuda.current_stream()
+    lib = nt._lib
+
+    def step(phases=7):
+        lib.call("nttmul_polymul_fused_rns_phases", C.data_ptr(), A.data_ptr(), B.data_ptr(),
+                 limbs.data_ptr(), fwd.data_ptr(), inv.data_ptr(), args.log_n, L, Bn,
+                 basis.mode, W.data_ptr(), phases, stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    # ---- timed region: K full steps ----
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    # per-kernel breakdown (same stream, events between the three launches)
+    log_n1 = max(args.log_n - 12, 0)
+    phase_ms = {}
+    names = {1: "col_fwd", 2: "row_fused", 4: "col_inv"} if log_n1 else {2: "row_fused"}
+    evs = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for k in names}
+    for _ in range(args.steps):
+        for k in names:
+            evs[k][0].record(stream)
+            step(k)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        for k, nm in names.items():
+            phase_ms[nm] = phase_ms.get(nm, 0.0) + evs[k][0].elapsed_time(evs[k][1])
+    phase_ms = {k: v / args.steps for k, v in phase_ms.items()}
+
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    value = world * Bn * args.steps / (ms_max / 1e3)
+
+    # ---- int-pipe and HBM roofs (live microbenchmarks) ----
+    roof = modmul_roof(nt, basis, stream)
+    hbm_peak, hbm_kind = peak_hbm()
+    products_per_step = Bn * L
+    row_ms = phase_ms["row_fused"]
+    row_rate = products_per_step * row_kernel_modmuls(n) / (row_ms / 1e3) / 1e9
+    all_rate = products_per_step * modmuls_per_product(n) / (ms_per_step / 1e3) / 1e9
+    traffic = load_traffic("row_fused")
+    roofline = {
+        "bound": "int", "kernel": "row_fused (fwd row stages a,b + Karatsuba middle + inv row stages)",
+        "achieved": round(row_rate, 2), "peak": round(roof["peak"], 2), "unit": "Gmodmul/s",
+        "frac": round(row_rate / roof["peak"], 4), "traffic": traffic,
+        "peak_source": roof["source"],
+        "step_achieved": round(all_rate, 2), "step_frac": round(all_rate / roof["peak"], 4),
+        "hbm": {
+            "algorithmic_bytes_per_step": products_per_step * 24 * n,
+            "achieved_gbs": round(products_per_step * 24 * n / (ms_per_step / 1e3) / 1e9, 1),
+            "peak_gbs": hbm_peak, "peak_source": hbm_kind,
+            "frac": round(products_per_step * 24 * n / (ms_per_step / 1e3) / 1e9 / hbm_peak, 4),
+        },
+        "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
+    }
+
+    # ---- e2e: public API with pinned host buffers, copies inside timing ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(nt, basis, A_h, B_h, args, world, stream)
+
+    # ---- parity spot check + CPU baseline (rank 0, N=1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        rate, kind, cores, sample, first = cpu_reference_rate(
+            primes, psis, n, A_h, B_h, args.cpu_seconds, threads)
+        step()
+        torch.cuda.synchronize()
+        assert np.array_equal(C[0].cpu().numpy(), first), "GPU != reference CPU (ct 0)"
+        cpu = {"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": sample, "parity_ct0": "bit-exact"}
+
+    ntt_us = ntt_latency_us(nt, basis.plans[0]) if rank == 0 else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic uniform residues (numpy default_rng), "
+                                   "primes/psi = reference RnsBasis.build(65536, 60, 21, seed=0)",
+            "config": {"workload": f"cfg3: fused negacyclic polymul, N=2^{args.log_n}, "
+                                   f"{L} x 60-bit RNS limbs",
+                       "batch_per_gpu": Bn, "global_batch": Bn * world, "n": n, "limbs": L,
+                       "parallelism": f"shard-by-ciphertext x{world}",
+                       "l2": "inputs 2x%.0f MiB > 126 MB L2, no flush" % (A.numel() * 8 / 2**20)},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "ntt_us": ntt_us, "gpu_launches": args.steps * (3 if log_n1 else 1),
+            "clocks": clk.summary(), "impl": "ours",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(nt, basis, A_h, B_h, args, world, stream):
+    import torch
+
+    Ap = torch.from_numpy(A_h).pin_memory()
+    Bp = torch.from_numpy(B_h).pin_memory()
+    Cp = torch.empty_like(Ap).pin_memory()
+    Ad, Bd = torch.empty_like(Ap, device="cuda"), torch.empty_like(Bp, device="cuda")
+    Cd, Wd = torch.empty_like(Ad), torch.empty_like(Ad)
+
+    def one():
+        Ad.copy_(Ap, non_blocking=True)
+        Bd.copy_(Bp, non_blocking=True)
+        nt.polymul_rns_batch(Ad, Bd, basis, out=Cd, workspace=Wd)
+        Cp.copy_(Cd, non_blocking=True)
+
+    steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": round(world * A_h.shape[0] * steps / (ms / 1e3), 2), "unit": UNIT,
+            "h2d_bytes_per_step": int(A_h.nbytes + B_h.nbytes),
+            "d2h_bytes_per_step": int(A_h.nbytes), "steps": steps,
+            "path": "polymul_rns_batch(pinned host -> HBM -> C ABI -> pinned host)"}
+
+
+def modmul_roof(nt, basis, stream):
+    """Register-resident modmul throughput (nttmul_modmul_roof), best variant."""
+    import ctypes
+
+    import torch
+
+    limb = basis.plans[0].limb()
+    sink = torch.zeros(1, dtype=torch.uint64, device="cuda")
+    best = {}
+    for kind, label in ((1, "shoup"), (0, "barrett_proposed")):
+        cnt = ctypes.c_double()
+        args = (ctypes.byref(limb), kind, 148 * 8, 256, 2000, sink.data_ptr(),
+                ctypes.byref(cnt), stream.cuda_stream)
+        nt._lib.call("nttmul_modmul_roof", *args)  # warm
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            nt._lib.call("nttmul_modmul_roof", *args)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        best[label] = 5 * cnt.value / (e0.elapsed_time(e1) / 1e3) / 1e9
+    lab = max(best, key=best.get)
+    return {"peak": best[lab],
+            "source": f"live nttmul_modmul_roof, best of {best} Gmodmul/s ({lab})"}
+
+
+def peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def load_traffic(kernel: str):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def ntt_latency_us(nt, plan):
+    """Standalone ntt_ct latency, one limb (N=2^16), device-resident."""
+    import torch
+
+    x = torch.zeros(plan.n, dtype=torch.uint64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(5):
+        nt.kernels.ntt_ct(x, plan.tw_fwd, *plan.red_args, False, None)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(50):
+        nt.kernels.ntt_ct(x, plan.tw_fwd, *plan.red_args, False, None)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return round(e0.elapsed_time(e1) * 1e3 / 50, 2)
+
+
+def run_reference(args, rank, world):
+    """The reference's own CPU implementation on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+
+    import oracle
+
+    n, L = 1 << args.log_n, args.limbs
+    nt = oracle.reference()
+    if nt is not None:
+        basis = nt.RnsBasis.build(n, 60, L, seed=0)
+        primes, psis = list(basis.primes), [p.psi for p in basis.plans]
+    else:  # reference not built: same primes via this package's host plan layer
+        import paper_2209_01290_b200.params as P
+
+        basis = None
+        primes, psis, s = [], [], 0
+        while len(primes) < L:
+            q = P.generate_prime(60, n, s)
+            s += 1
+            if q not in primes:
+                primes.append(q)
+                psis.append(P.find_primitive_root(q, 2 * n, 0))
+    A = make_inputs(primes, 2, n, seed=1000)
+    B = make_inputs(primes, 2, n, seed=2000)
+    threads = len(os.sched_getaffinity(0))
+    per_step = max(2.0, 60.0 / max(args.steps + args.warmup, 1))
+    rates = []
+    for i in range(args.warmup + args.steps):
+        rate, kind, cores, sample, _ = cpu_reference_rate(primes, psis, n, A, B, per_step,
+                                                          threads)
+        if i >= args.warmup:
+            rates.append(rate)
+    value = sum(rates) / len(rates)
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 / value, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic uniform residues",
+            "config": {"workload": f"cfg3: fused negacyclic polymul, N=2^{args.log_n}, "
+                                   f"{L} x 60-bit RNS limbs", "n": n, "limbs": L},
+            "impl": "reference",
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
+                             "kind": kind, "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,529 @@
+// capi.cu - extern "C" entry points (include/nttmul_b200.h) and launchers.
+//
+// Every function validates sizes, alignment and device-pointer-ness, launches
+// on the caller's stream and returns a status code; it never aborts and never
+// synchronizes (except where documented).  Reference interfaces replaced are
+// cited per function in the header.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "nttmul_b200.h"
+#include "ntt_kernels.cuh"
+
+using namespace nttb;
+
+namespace {
+
+thread_local char g_err[256] = "";
+
+int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_status(const char *what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return NTTMUL_OK;
+  return fail(NTTMUL_ELAUNCH, "%s: %s", what, cudaGetErrorString(e));
+}
+
+typedef unsigned __int128 u128;
+
+inline u64 mulmod_host(u64 a, u64 b, u64 q) {
+  return static_cast<u64>((static_cast<u128>(a) * b) % q);
+}
+inline u64 shoup_host(u64 w, u64 q) {
+  return static_cast<u64>((static_cast<u128>(w) << 64) / q);
+}
+inline int bitlen(u64 x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+int check_dev(const void *p, size_t align, const char *name) {
+  if (!p) return fail(NTTMUL_EPTR, "%s is NULL", name);
+  if (reinterpret_cast<uintptr_t>(p) % align)
+    return fail(NTTMUL_EALIGN, "%s not %zu-byte aligned", name, align);
+  cudaPointerAttributes at;
+  const cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(NTTMUL_EPTR, "%s: %s", name, cudaGetErrorString(e));
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return fail(NTTMUL_EPTR, "%s is not device memory", name);
+  return NTTMUL_OK;
+}
+
+#define CHECK(x)                    \
+  do {                              \
+    const int _s = (x);             \
+    if (_s != NTTMUL_OK) return _s; \
+  } while (0)
+
+inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+
+inline unsigned grid_for(long long n, int threads, long long cap = 148LL * 64) {
+  long long g = (n + threads - 1) / threads;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+// ---- dynamic shared memory opt-in (once per kernel instantiation) --------
+template <class K>
+int smem_optin(K kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return NTTMUL_OK;
+  const cudaError_t e = cudaFuncSetAttribute(
+      kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e != cudaSuccess)
+    return fail(NTTMUL_ECUDA, "smem opt-in %zu B: %s", bytes, cudaGetErrorString(e));
+  return NTTMUL_OK;
+}
+
+// ---- row kernel dispatch ---------------------------------------------------
+template <int LOG_R, int FWD, bool MID, int INV, int MODE>
+int launch_row_t(const RowParams &P, long long rows, cudaStream_t st) {
+  constexpr int NP = MID ? 2 : 1;
+  const size_t smem = NP * RowGeom<LOG_R>::PADN * sizeof(u64);
+  auto k = row_kernel<LOG_R, FWD, MID, INV, MODE>;
+  CHECK(smem_optin(k, smem));
+  k<<<static_cast<unsigned>(rows), RowGeom<LOG_R>::T, smem, st>>>(P);
+  return cuda_status("row_kernel");
+}
+
+template <int FWD, bool MID, int INV, int MODE>
+int launch_row_m(int log_r, const RowParams &P, long long rows, cudaStream_t st) {
+  switch (log_r) {
+    case 10: return launch_row_t<10, FWD, MID, INV, MODE>(P, rows, st);
+    case 11: return launch_row_t<11, FWD, MID, INV, MODE>(P, rows, st);
+    case 12: return launch_row_t<12, FWD, MID, INV, MODE>(P, rows, st);
+  }
+  return fail(NTTMUL_EINVAL, "row size 2^%d unsupported", log_r);
+}
+
+// ---- column kernel dispatch -------------------------------------------------
+template <bool INV>
+int launch_col(int log_n1, const ColParams &P, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>(
+      (P.nsrc * (P.npolys << COL_LOG_R) + COL_THREADS - 1) / COL_THREADS);
+  switch (log_n1) {
+    case 1: col_kernel<1, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 2: col_kernel<2, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 3: col_kernel<3, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 4: col_kernel<4, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 5: col_kernel<5, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
+    default: return fail(NTTMUL_EINVAL, "column count 2^%d unsupported", log_n1);
+  }
+  return cuda_status("col_kernel");
+}
+
+// ---- small kernel -----------------------------------------------------------
+int launch_small(const SmallParams &P, int mode, long long npolys, cudaStream_t st) {
+  const int n = 1 << P.log_n;
+  const int threads = n / 2 < 32 ? 32 : (n / 2 > 256 ? 256 : n / 2);
+  const size_t smem = (P.mid ? 2 : 1) * static_cast<size_t>(n) * sizeof(u64);
+  switch (mode) {
+    case 0: CHECK(smem_optin(small_kernel<0>, smem));
+      small_kernel<0><<<static_cast<unsigned>(npolys), threads, smem, st>>>(P); break;
+    case 1: CHECK(smem_optin(small_kernel<1>, smem));
+      small_kernel<1><<<static_cast<unsigned>(npolys), threads, smem, st>>>(P); break;
+    default: CHECK(smem_optin(small_kernel<2>, smem));
+      small_kernel<2><<<static_cast<unsigned>(npolys), threads, smem, st>>>(P); break;
+  }
+  return cuda_status("small_kernel");
+}
+
+constexpr int SMALL_MAX_LOG = 9;  // n <= 2^9 -> small kernel
+
+// ---- composite transforms -----------------------------------------------------
+int run_forward(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
+                long long npolys, bool truncate, cudaStream_t st) {
+  if (npolys == 0) return NTTMUL_OK;
+  if (log_n <= SMALL_MAX_LOG) {
+    SmallParams P{a, a, nullptr, tw, ls, log_n, truncate ? FWD_TRUNC : FWD_FULL, 0,
+                  INV_NONE, FIN_PLAIN};
+    return launch_small(P, NTTMUL_RED_ONE_SUB, npolys, st);
+  }
+  const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
+  const int log_n1 = log_n - log_r;
+  if (log_n1 > 0) {
+    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, FIN_LAZY};
+    CHECK(launch_col<false>(log_n1, C, st));
+  }
+  RowParams R{a, a, nullptr, tw, ls, log_n1, FIN_PLAIN};
+  const long long rows = npolys << log_n1;
+  return truncate ? launch_row_m<FWD_TRUNC, false, INV_NONE, 2>(log_r, R, rows, st)
+                  : launch_row_m<FWD_FULL, false, INV_NONE, 2>(log_r, R, rows, st);
+}
+
+int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
+                long long npolys, bool skip, int fin, cudaStream_t st) {
+  if (npolys == 0) return NTTMUL_OK;
+  if (log_n <= SMALL_MAX_LOG) {
+    SmallParams P{a, a, nullptr, tw, ls, log_n, FWD_NONE, 0, skip ? INV_SKIP : INV_FULL,
+                  fin};
+    return launch_small(P, NTTMUL_RED_ONE_SUB, npolys, st);
+  }
+  const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
+  const int log_n1 = log_n - log_r;
+  RowParams R{a, a, nullptr, tw, ls, log_n1, fin};
+  const long long rows = npolys << log_n1;
+  CHECK((skip ? launch_row_m<FWD_NONE, false, INV_SKIP, 2>(log_r, R, rows, st)
+              : launch_row_m<FWD_NONE, false, INV_FULL, 2>(log_r, R, rows, st)));
+  if (log_n1 > 0) {
+    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, fin};
+    CHECK(launch_col<true>(log_n1, C, st));
+  }
+  return NTTMUL_OK;
+}
+
+// phases: bit 0 = forward column pass, bit 1 = row kernel, bit 2 = inverse
+// column pass (n > 4096 only; smaller n always runs as one row kernel).
+template <int MODE>
+int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
+                  const LimbSet &ls, int log_n, long long npolys, int phases,
+                  cudaStream_t st) {
+  if (npolys == 0) return NTTMUL_OK;
+  if (log_n <= SMALL_MAX_LOG) {
+    if (!(phases & 2)) return NTTMUL_OK;
+    SmallParams P{c, a, b, tw, ls, log_n, FWD_TRUNC, 1, INV_SKIP, FIN_SCALED_SKIP};
+    return launch_small(P, MODE, npolys, st);
+  }
+  const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
+  const int log_n1 = log_n - log_r;
+  const u64 *in0 = a, *in1 = b;
+  if (log_n1 > 0) {
+    if (phases & 1) {
+      ColParams C{a, b, c, ws, 2, npolys, tw, ls, FIN_LAZY};
+      CHECK(launch_col<false>(log_n1, C, st));
+    }
+    in0 = c;
+    in1 = ws;
+  }
+  if (phases & 2) {
+    RowParams R{c, in0, in1, tw, ls, log_n1, FIN_SCALED_SKIP};
+    CHECK((launch_row_m<FWD_TRUNC, true, INV_SKIP, MODE>(log_r, R, npolys << log_n1, st)));
+  }
+  if (log_n1 > 0 && (phases & 4)) {
+    ColParams C{c, nullptr, c, nullptr, 1, npolys, tw, ls, FIN_SCALED_SKIP};
+    CHECK(launch_col<true>(log_n1, C, st));
+  }
+  return NTTMUL_OK;
+}
+
+int run_polymul(int mode, u64 *c, const u64 *a, const u64 *b, u64 *ws,
+                const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
+                int phases, cudaStream_t st) {
+  switch (mode) {
+    case 0: return run_polymul_m<0>(c, a, b, ws, tw, ls, log_n, npolys, phases, st);
+    case 1: return run_polymul_m<1>(c, a, b, ws, tw, ls, log_n, npolys, phases, st);
+    default: return run_polymul_m<2>(c, a, b, ws, tw, ls, log_n, npolys, phases, st);
+  }
+}
+
+int check_log_n(int log_n, int min_log) {
+  if (log_n < min_log || log_n > NTTMUL_MAX_LOG_N)
+    return fail(NTTMUL_EINVAL, "log_n=%d outside [%d, %d]", log_n, min_log,
+                NTTMUL_MAX_LOG_N);
+  return NTTMUL_OK;
+}
+
+// one-prime limb from the reference's (q, mode, mu, s_in, s_out); the scale
+// constants use w1_inv when given (inverse transforms)
+int single_limb(Limb *L, u64 q, int mode, u64 mu, int s_in, int s_out,
+                int log_n, u64 w1_inv) {
+  return nttmul_limb_prepare(L, q, mode, mu, s_in, s_out, log_n, w1_inv);
+}
+
+TwSet one_table(const u64 *pairs) {
+  const ulonglong2 *t = reinterpret_cast<const ulonglong2 *>(pairs);
+  return TwSet{t, t, 0};
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+int nttmul_abi_version(void) { return 1; }
+
+const char *nttmul_last_error(void) { return g_err; }
+
+int nttmul_limb_prepare(nttmul_limb_t *out, uint64_t q, int mode, uint64_t mu,
+                        int s_in, int s_out, int log_n, uint64_t w1_inv) {
+  if (!out) return fail(NTTMUL_EINVAL, "limb output is NULL");
+  if (q < 3 || !(q & 1)) return fail(NTTMUL_EINVAL, "modulus %llu must be odd and >= 3",
+                                     static_cast<unsigned long long>(q));
+  const int m = bitlen(q);
+  if (m > 62) return fail(NTTMUL_EINVAL, "modulus has %d bits; at most 62 supported", m);
+  if (log_n < 1 || log_n > NTTMUL_MAX_LOG_N) return fail(NTTMUL_EINVAL, "log_n=%d", log_n);
+  std::memset(out, 0, sizeof(*out));
+  out->q = q;
+  out->mode = static_cast<uint32_t>(mode);
+  out->log_n = static_cast<uint32_t>(log_n);
+  if (mode == NTTMUL_RED_BUILTIN) {
+    out->mu_sh = 0;
+    out->s_in = 0;
+    out->s_hi = 0;
+  } else if (mode == NTTMUL_RED_TWO_SUB || mode == NTTMUL_RED_ONE_SUB) {
+    if (s_in < 0 || s_in > 63 || s_out < 1 || s_out > 127)
+      return fail(NTTMUL_EINVAL, "shifts s_in=%d s_out=%d out of range", s_in, s_out);
+    if (s_out <= 64) {
+      const int sh = 64 - s_out;
+      if (sh && (mu >> (64 - sh))) return fail(NTTMUL_EINVAL, "mu too wide for s_out=%d", s_out);
+      out->mu_sh = mu << sh;
+      out->s_hi = 0;
+    } else {
+      out->mu_sh = mu;
+      out->s_hi = static_cast<uint32_t>(s_out - 64);
+    }
+    out->s_in = static_cast<uint32_t>(s_in);
+  } else {
+    return fail(NTTMUL_EINVAL, "unknown reduction mode %d", mode);
+  }
+  // 2^-k mod q = ((q+1)/2)^k
+  const u64 half = (q + 1) >> 1;
+  u64 f_full = 1, f_skip = 1;
+  for (int i = 0; i < log_n; ++i) f_full = mulmod_host(f_full, half, q);
+  for (int i = 0; i < log_n - 1; ++i) f_skip = mulmod_host(f_skip, half, q);
+  const u64 w1 = w1_inv % q;
+  const u64 g_full = mulmod_host(w1, f_full, q), g_skip = mulmod_host(w1, f_skip, q);
+  const u64 full[4] = {f_full, shoup_host(f_full, q), g_full, shoup_host(g_full, q)};
+  const u64 skip[4] = {f_skip, shoup_host(f_skip, q), g_skip, shoup_host(g_skip, q)};
+  std::memcpy(out->sc_full, full, sizeof(full));
+  std::memcpy(out->sc_skip, skip, sizeof(skip));
+  return NTTMUL_OK;
+}
+
+int nttmul_twiddle_tables(uint64_t *tw_fwd, uint64_t *tw_inv, uint64_t *fwd_pairs,
+                          uint64_t *inv_pairs, uint64_t q, uint64_t psi,
+                          uint64_t psi_inv, int log_n, void *stream) {
+  CHECK(check_log_n(log_n, 1));
+  if (psi >= q || psi_inv >= q) return fail(NTTMUL_EINVAL, "psi not reduced");
+  if (tw_fwd) CHECK(check_dev(tw_fwd, 8, "tw_fwd"));
+  if (tw_inv) CHECK(check_dev(tw_inv, 8, "tw_inv"));
+  if (fwd_pairs) CHECK(check_dev(fwd_pairs, 16, "fwd_pairs"));
+  if (inv_pairs) CHECK(check_dev(inv_pairs, 16, "inv_pairs"));
+  const int m = bitlen(q);
+  Limb L;
+  CHECK(nttmul_limb_prepare(&L, q, NTTMUL_RED_ONE_SUB,
+                            static_cast<u64>((static_cast<u128>(1) << (2 * m + 1)) / q),
+                            m - 2, m + 3, log_n, 1));
+  const long long n = 1LL << log_n;
+  twiddle_kernel<<<grid_for(n, 256, 1LL << 30), 256, 0, S(stream)>>>(
+      tw_fwd, tw_inv, reinterpret_cast<ulonglong2 *>(fwd_pairs),
+      reinterpret_cast<ulonglong2 *>(inv_pairs), psi, psi_inv, log_n, L);
+  return cuda_status("twiddle_kernel");
+}
+
+int nttmul_shoup_pairs(uint64_t *pairs, const uint64_t *tw, uint64_t q, int64_t n,
+                       void *stream) {
+  if (n < 0) return fail(NTTMUL_EINVAL, "n < 0");
+  if (n == 0) return NTTMUL_OK;
+  if (q < 3 || bitlen(q) > 62) return fail(NTTMUL_EINVAL, "bad modulus");
+  CHECK(check_dev(pairs, 16, "pairs"));
+  CHECK(check_dev(tw, 8, "tw"));
+  shoup_pairs_kernel<<<grid_for(n, 256, 1LL << 30), 256, 0, S(stream)>>>(
+      reinterpret_cast<ulonglong2 *>(pairs), tw, q, n);
+  return cuda_status("shoup_pairs_kernel");
+}
+
+int nttmul_check_twiddles(const uint64_t *tw_fwd, const uint64_t *tw_inv, uint64_t q,
+                          int64_t n, uint64_t *bad_out, void *stream) {
+  if (n < 1) return fail(NTTMUL_EINVAL, "n < 1");
+  CHECK(check_dev(tw_fwd, 8, "tw_fwd"));
+  CHECK(check_dev(tw_inv, 8, "tw_inv"));
+  CHECK(check_dev(bad_out, 8, "bad_out"));
+  Limb L;
+  std::memset(&L, 0, sizeof(L));
+  L.q = q;
+  if (cudaMemsetAsync(bad_out, 0, 8, S(stream)) != cudaSuccess)
+    return cuda_status("memset");
+  check_twiddles_kernel<<<grid_for(n, 256, 1LL << 30), 256, 0, S(stream)>>>(
+      tw_fwd, tw_inv, n, reinterpret_cast<unsigned long long *>(bad_out), L);
+  return cuda_status("check_twiddles_kernel");
+}
+
+int nttmul_ntt_ct(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, int mode,
+                  uint64_t mu, int s_in, int s_out, int truncate, int log_n,
+                  int64_t batch, void *stream) {
+  CHECK(check_log_n(log_n, 1));
+  if (batch < 0) return fail(NTTMUL_EINVAL, "batch < 0");
+  if (batch == 0) return NTTMUL_OK;
+  CHECK(check_dev(a, 8, "a"));
+  CHECK(check_dev(tw_pairs, 16, "tw_pairs"));
+  LimbSet ls;
+  ls.table = nullptr;
+  ls.num = 1;
+  CHECK(single_limb(&ls.single, q, mode, mu, s_in, s_out, log_n, 1));
+  return run_forward(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0, S(stream));
+}
+
+int nttmul_intt_gs(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, uint64_t half_q,
+                   int mode, uint64_t mu, int s_in, int s_out, int scaled,
+                   int skip_first, int log_n, int64_t batch, uint64_t w1_inv,
+                   void *stream) {
+  CHECK(check_log_n(log_n, 1));
+  if (batch < 0) return fail(NTTMUL_EINVAL, "batch < 0");
+  if (half_q != (q + 1) / 2) return fail(NTTMUL_EINVAL, "half_q != (q+1)/2");
+  if (batch == 0) return NTTMUL_OK;
+  CHECK(check_dev(a, 8, "a"));
+  CHECK(check_dev(tw_pairs, 16, "tw_pairs"));
+  LimbSet ls;
+  ls.table = nullptr;
+  ls.num = 1;
+  CHECK(single_limb(&ls.single, q, mode, mu, s_in, s_out, log_n, w1_inv));
+  const int fin = scaled ? (skip_first ? FIN_SCALED_SKIP : FIN_SCALED_FULL) : FIN_PLAIN;
+  return run_inverse(a, one_table(tw_pairs), ls, log_n, batch, skip_first != 0, fin,
+                     S(stream));
+}
+
+int nttmul_fused_middle(const uint64_t *ah, const uint64_t *bh, uint64_t *ch,
+                        const uint64_t *tw_pairs, uint64_t q, int mode, uint64_t mu,
+                        int s_in, int s_out, int log_n, int64_t batch, void *stream) {
+  CHECK(check_log_n(log_n, 2));
+  if (batch < 0) return fail(NTTMUL_EINVAL, "batch < 0");
+  if (batch == 0) return NTTMUL_OK;
+  CHECK(check_dev(ah, 8, "ah"));
+  CHECK(check_dev(bh, 8, "bh"));
+  CHECK(check_dev(ch, 8, "ch"));
+  CHECK(check_dev(tw_pairs, 16, "tw_pairs"));
+  Limb L;
+  CHECK(single_limb(&L, q, mode, mu, s_in, s_out, log_n, 1));
+  const long long npairs = batch << (log_n - 1);
+  const ulonglong2 *tw = reinterpret_cast<const ulonglong2 *>(tw_pairs);
+  const unsigned g = grid_for(npairs, 256);
+  switch (mode) {
+    case 0: fused_middle_kernel<0><<<g, 256, 0, S(stream)>>>(ah, bh, ch, tw, log_n, npairs, L); break;
+    case 1: fused_middle_kernel<1><<<g, 256, 0, S(stream)>>>(ah, bh, ch, tw, log_n, npairs, L); break;
+    default: fused_middle_kernel<2><<<g, 256, 0, S(stream)>>>(ah, bh, ch, tw, log_n, npairs, L); break;
+  }
+  return cuda_status("fused_middle_kernel");
+}
+
+int nttmul_hadamard(const uint64_t *a, const uint64_t *b, uint64_t *out, int64_t n,
+                    uint64_t q, int mode, uint64_t mu, int s_in, int s_out,
+                    void *stream) {
+  if (n < 0) return fail(NTTMUL_EINVAL, "n < 0");
+  if (n == 0) return NTTMUL_OK;
+  CHECK(check_dev(a, 8, "a"));
+  CHECK(check_dev(b, 8, "b"));
+  CHECK(check_dev(out, 8, "out"));
+  Limb L;
+  CHECK(single_limb(&L, q, mode, mu, s_in, s_out, 1, 1));
+  const unsigned g = grid_for(n, 256);
+  switch (mode) {
+    case 0: hadamard_kernel<0><<<g, 256, 0, S(stream)>>>(a, b, out, n, L); break;
+    case 1: hadamard_kernel<1><<<g, 256, 0, S(stream)>>>(a, b, out, n, L); break;
+    default: hadamard_kernel<2><<<g, 256, 0, S(stream)>>>(a, b, out, n, L); break;
+  }
+  return cuda_status("hadamard_kernel");
+}
+
+int nttmul_scale(uint64_t *a, uint64_t factor, int64_t n, uint64_t q, int mode,
+                 uint64_t mu, int s_in, int s_out, void *stream) {
+  if (n < 0) return fail(NTTMUL_EINVAL, "n < 0");
+  if (n == 0) return NTTMUL_OK;
+  CHECK(check_dev(a, 8, "a"));
+  Limb L;
+  CHECK(single_limb(&L, q, mode, mu, s_in, s_out, 1, 1));
+  const unsigned g = grid_for(n, 256);
+  switch (mode) {
+    case 0: scale_kernel<0><<<g, 256, 0, S(stream)>>>(a, factor, n, L); break;
+    case 1: scale_kernel<1><<<g, 256, 0, S(stream)>>>(a, factor, n, L); break;
+    default: scale_kernel<2><<<g, 256, 0, S(stream)>>>(a, factor, n, L); break;
+  }
+  return cuda_status("scale_kernel");
+}
+
+int nttmul_mulmod_loop(const uint64_t *a, const uint64_t *b, int64_t n, uint64_t q,
+                       int mode, uint64_t mu, int s_in, int s_out, uint64_t passes,
+                       uint64_t *sink_out, void *stream) {
+  if (n < 0) return fail(NTTMUL_EINVAL, "n < 0");
+  CHECK(check_dev(sink_out, 8, "sink_out"));
+  if (cudaMemsetAsync(sink_out, 0, 8, S(stream)) != cudaSuccess)
+    return cuda_status("memset");
+  if (n == 0 || passes == 0) return NTTMUL_OK;
+  CHECK(check_dev(a, 8, "a"));
+  CHECK(check_dev(b, 8, "b"));
+  Limb L;
+  CHECK(single_limb(&L, q, mode, mu, s_in, s_out, 1, 1));
+  const unsigned g = grid_for(n, 256);
+  switch (mode) {
+    case 0: mulmod_loop_kernel<0><<<g, 256, 0, S(stream)>>>(a, b, n, passes, sink_out, L); break;
+    case 1: mulmod_loop_kernel<1><<<g, 256, 0, S(stream)>>>(a, b, n, passes, sink_out, L); break;
+    default: mulmod_loop_kernel<2><<<g, 256, 0, S(stream)>>>(a, b, n, passes, sink_out, L); break;
+  }
+  return cuda_status("mulmod_loop_kernel");
+}
+
+int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64_t *b,
+                                    const nttmul_limb_t *limbs, const uint64_t *fwd_pairs,
+                                    const uint64_t *inv_pairs, int log_n, int num_limbs,
+                                    int64_t batch, int mode, uint64_t *workspace,
+                                    int phases, void *stream) {
+  CHECK(check_log_n(log_n, 2));
+  if (num_limbs < 1) return fail(NTTMUL_EINVAL, "num_limbs < 1");
+  if (batch < 0) return fail(NTTMUL_EINVAL, "batch < 0");
+  if (batch == 0) return NTTMUL_OK;
+  CHECK(check_dev(c, 8, "c"));
+  CHECK(check_dev(a, 8, "a"));
+  CHECK(check_dev(b, 8, "b"));
+  CHECK(check_dev(limbs, 8, "limbs"));
+  CHECK(check_dev(fwd_pairs, 16, "fwd_pairs"));
+  CHECK(check_dev(inv_pairs, 16, "inv_pairs"));
+  if (log_n > COL_LOG_R) {
+    CHECK(check_dev(workspace, 8, "workspace"));
+    if (workspace == a || workspace == c)
+      return fail(NTTMUL_EINVAL, "workspace may not alias a or c");
+  }
+  if (c == b && log_n > COL_LOG_R)
+    return fail(NTTMUL_EINVAL, "c may not alias b");
+  if (mode < 0 || mode > 2) return fail(NTTMUL_EINVAL, "unknown reduction mode %d", mode);
+  LimbSet ls;
+  ls.table = limbs;
+  ls.num = num_limbs;
+  std::memset(&ls.single, 0, sizeof(ls.single));
+  const long long stride = 1LL << log_n;
+  TwSet tw{reinterpret_cast<const ulonglong2 *>(fwd_pairs),
+           reinterpret_cast<const ulonglong2 *>(inv_pairs), stride};
+  return run_polymul(mode, c, a, b, workspace, tw, ls, log_n,
+                     batch * num_limbs, phases, S(stream));
+}
+
+int nttmul_polymul_fused_rns(uint64_t *c, const uint64_t *a, const uint64_t *b,
+                             const nttmul_limb_t *limbs, const uint64_t *fwd_pairs,
+                             const uint64_t *inv_pairs, int log_n, int num_limbs,
+                             int64_t batch, int mode, uint64_t *workspace,
+                             void *stream) {
+  return nttmul_polymul_fused_rns_phases(c, a, b, limbs, fwd_pairs, inv_pairs, log_n,
+                                         num_limbs, batch, mode, workspace, 7, stream);
+}
+
+int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int threads,
+                       int64_t iters, uint64_t *sink_out, double *modmuls_out,
+                       void *stream) {
+  if (!limb_host || blocks < 1 || threads < 32 || threads > 256 || iters < 1)
+    return fail(NTTMUL_EINVAL, "bad microbenchmark geometry");
+  CHECK(check_dev(sink_out, 8, "sink_out"));
+  constexpr int CH = 8;
+  const Limb L = *limb_host;
+  const u64 w = (L.q >> 1) | 1, wp = shoup_host(w, L.q);
+  if (kind == 1) {
+    modmul_roof_kernel<1, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
+  } else {
+    switch (L.mode) {
+      case 0: modmul_roof_kernel<0, 0, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp); break;
+      case 1: modmul_roof_kernel<0, 1, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp); break;
+      default: modmul_roof_kernel<0, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp); break;
+    }
+  }
+  if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * CH;
+  return cuda_status("modmul_roof_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,510 @@
+// ntt_kernels.cuh - the sm_100a kernels of the polymul hot path.
+//
+// Data layout in HBM: polynomials are uint64[n], back to back ([batch, n] or
+// [batch, limbs, n]); twiddles are {w, w'} pairs, one [n] table per prime.
+//
+// Large transforms (n = 2^13 .. 2^17) use a stage-grouped 2D split
+// n = N1 x N2 with N2 = 4096 (one "row"): the merged-CT stages with half-size
+// k >= N2 act independently on each column j mod N2 and need only the N1-1
+// twiddles tw[1..N1), so the COLUMN kernel gives each thread one column in
+// registers (coalesced across threads); the remaining stages stay inside a
+// contiguous row, which the ROW kernel keeps in shared memory and registers
+// (two 4-stage register passes + one 16-consecutive-element tail).  The
+// inverse is the mirror (row kernel first, then column kernel).  The fused
+// polymul is COL(a,b) -> ROW(fwd a,b + Karatsuba middle + inverse) -> COL^-1.
+// Output order and values are exactly the reference's merged transforms
+// (reference _kernels.pyx:52-129): only the schedule of the same butterflies
+// changes.  Transforms with n <= 2^12 need no column kernel; n < 2^10 uses the
+// simple one-CTA-per-polynomial kernel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "radix.cuh"
+
+namespace nttb {
+
+struct TwSet {
+  const ulonglong2 *fwd;  // table of limb 0
+  const ulonglong2 *inv;
+  long long stride;       // entries between consecutive limbs (0: one prime)
+};
+
+struct LimbSet {
+  const Limb *table;  // device [num] or nullptr -> use `single`
+  Limb single;
+  int num;
+};
+
+__device__ __forceinline__ Limb get_limb(const LimbSet &S, long long poly,
+                                         int &limb) {
+  if (S.table) {
+    limb = static_cast<int>(poly % S.num);
+    return S.table[limb];
+  }
+  limb = 0;
+  return S.single;
+}
+
+// padded shared-memory index: one u64 of padding per 16 keeps both the
+// strided head passes and the 16-consecutive tail pass at the 2-wavefront
+// minimum for 64-bit accesses.
+__device__ __forceinline__ int pad(int o) { return o + (o >> 4); }
+
+enum FwdKind { FWD_NONE = 0, FWD_FULL = 1, FWD_TRUNC = 2 };
+enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
+
+// ---------------------------------------------------------------------------
+// ROW kernel
+
+template <int LOG_R>
+struct RowGeom {
+  static constexpr int N2 = 1 << LOG_R;
+  static constexpr int T = N2 / 16;                // threads; 16 elems each
+  static constexpr int PADN = N2 + N2 / 16;        // padded row length
+  static constexpr int HEAD = LOG_R - 4;           // stages before the tail
+  static constexpr int R1 = (HEAD + 1) / 2;        // first head pass
+  static constexpr int R2 = HEAD - R1;             // second head pass
+  static_assert(R1 >= 1 && R1 <= 4 && R2 >= 1 && R2 <= 4, "row size");
+};
+
+struct RowParams {
+  u64 *out;
+  const u64 *in0;
+  const u64 *in1;
+  TwSet tw;
+  LimbSet limbs;
+  int log_n1;  // rows per polynomial = 2^log_n1
+  int fin;     // FinalMode of the global last inverse stage (if in this kernel)
+};
+
+// forward head pass: R stages starting at row-local stage S0
+template <int LOG_R, int S0, int R, int NP, bool FROM_GLOBAL>
+__device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
+                                         const u64 *__restrict__ g0,
+                                         const u64 *__restrict__ g1,
+                                         u64 rowbase,
+                                         const ulonglong2 *__restrict__ tw,
+                                         u64 q, u64 q2) {
+  constexpr int T = RowGeom<LOG_R>::T;
+  constexpr int PADN = RowGeom<LOG_R>::PADN;
+  constexpr int U = 16 >> R;           // units per thread
+  constexpr int LK = LOG_R - S0 - R;   // log2(k_last)
+#pragma unroll
+  for (int w = 0; w < U; ++w) {
+    const int u = threadIdx.x + w * T;
+    const int g = u >> LK;
+    const int o0 = (g << (LOG_R - S0)) + (u & ((1 << LK) - 1));
+    u64 x[NP][1 << R];
+#pragma unroll
+    for (int e = 0; e < (1 << R); ++e) {
+      const int o = o0 + (e << LK);
+      if (FROM_GLOBAL) {
+        x[0][e] = g0[o];
+        if (NP > 1) x[NP - 1][e] = g1[o];
+      } else {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) x[p][e] = sm[p * PADN + pad(o)];
+      }
+    }
+    fwd_radix<R, R, NP>(x, (rowbase << S0) + g, tw, q, q2);
+#pragma unroll
+    for (int e = 0; e < (1 << R); ++e) {
+      const int o = o0 + (e << LK);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) sm[p * PADN + pad(o)] = x[p][e];
+    }
+  }
+}
+
+// inverse head pass (mirror of head_fwd); TO_GLOBAL only for S0 == 0
+template <int LOG_R, int S0, int R, bool TO_GLOBAL>
+__device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
+                                         u64 *__restrict__ gout, u64 rowbase,
+                                         const ulonglong2 *__restrict__ tw,
+                                         const Limb &L, u64 q2, int fin) {
+  constexpr int T = RowGeom<LOG_R>::T;
+  constexpr int U = 16 >> R;
+  constexpr int LK = LOG_R - S0 - R;
+#pragma unroll
+  for (int w = 0; w < U; ++w) {
+    const int u = threadIdx.x + w * T;
+    const int g = u >> LK;
+    const int o0 = (g << (LOG_R - S0)) + (u & ((1 << LK) - 1));
+    u64 x[1][1 << R];
+#pragma unroll
+    for (int e = 0; e < (1 << R); ++e) x[0][e] = sm[pad(o0 + (e << LK))];
+    const u64 B0 = (rowbase << S0) + g;
+    if (TO_GLOBAL) {
+      inv_radix<R, R, 1, 1>(x, B0, tw, L.q, q2);
+      inv_stage0<R, 1>(x, B0, tw, L, q2, fin);
+#pragma unroll
+      for (int e = 0; e < (1 << R); ++e) gout[o0 + (e << LK)] = x[0][e];
+    } else {
+      inv_radix<R, R, 0, 1>(x, B0, tw, L.q, q2);
+#pragma unroll
+      for (int e = 0; e < (1 << R); ++e) sm[pad(o0 + (e << LK))] = x[0][e];
+    }
+  }
+}
+
+// tail pass: 16 consecutive elements per thread (row-local stages
+// LOG_R-4 .. LOG_R-1), optionally with the fused middle in between.
+template <int LOG_R, int NP, int FWD, bool MID, int INV, int MODE>
+__device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
+                                          const ulonglong2 *__restrict__ twf,
+                                          const ulonglong2 *__restrict__ twi,
+                                          const Limb &L, u64 q2) {
+  constexpr int PADN = RowGeom<LOG_R>::PADN;
+  const u64 q = L.q;
+  const int o0 = threadIdx.x * 16;
+  const u64 B0 = (rowbase << (LOG_R - 4)) + threadIdx.x;
+  u64 x[NP][16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) x[p][e] = sm[p * PADN + pad(o0 + e)];
+  if (FWD == FWD_FULL) fwd_radix<4, 4, NP>(x, B0, twf, q, q2);
+  if (FWD == FWD_TRUNC) fwd_radix<4, 3, NP>(x, B0, twf, q, q2);
+  if (MID) {
+    // pair p = (2p, 2p+1); twiddle tw[n/4 + i/2] == tw[4*B0 + p/2]; sign of
+    // the z term = parity of the global pair index = parity of p.
+    u64 c[1][16];
+#pragma unroll
+    for (int p = 0; p < 8; p += 2) {
+      const ulonglong2 w = ldtw(twf, 4 * B0 + (p >> 1));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i0 = 2 * (p + h);
+        fused_pair<MODE>(canon4(x[0][i0], q, q2), canon4(x[0][i0 + 1], q, q2),
+                         canon4(x[NP - 1][i0], q, q2),
+                         canon4(x[NP - 1][i0 + 1], q, q2), w.x, w.y, h != 0, L,
+                         c[0][i0], c[0][i0 + 1]);
+      }
+    }
+    inv_radix<4, 3, 0, 1>(c, B0, twi, q, q2);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) sm[pad(o0 + e)] = c[0][e];
+  } else {
+    if (INV == INV_FULL) inv_radix<4, 4, 0, NP>(x, B0, twi, q, q2);
+    if (INV == INV_SKIP) inv_radix<4, 3, 0, NP>(x, B0, twi, q, q2);
+    if (INV == INV_NONE) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+#pragma unroll
+        for (int p = 0; p < NP; ++p) x[p][e] = canon4(x[p][e], q, q2);
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) sm[p * PADN + pad(o0 + e)] = x[p][e];
+  }
+}
+
+template <int LOG_R, int FWD, bool MID, int INV, int MODE>
+__global__ void __launch_bounds__(1 << (LOG_R - 4))
+    row_kernel(const RowParams P) {
+  using G = RowGeom<LOG_R>;
+  constexpr int NP = MID ? 2 : 1;
+  extern __shared__ u64 sm[];
+  const long long row = blockIdx.x;
+  const long long poly = row >> P.log_n1;
+  const int r = static_cast<int>(row & ((1LL << P.log_n1) - 1));
+  int limb;
+  const Limb L = get_limb(P.limbs, poly, limb);
+  const u64 q = L.q, q2 = 2 * L.q;
+  const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
+  const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
+  const u64 rowbase = (1ULL << P.log_n1) + r;  // (N1 + r): group index base
+  const long long off = row * G::N2;
+
+  if (FWD != FWD_NONE) {
+    head_fwd<LOG_R, 0, G::R1, NP, true>(sm, P.in0 + off,
+                                        NP > 1 ? P.in1 + off : nullptr,
+                                        rowbase, twf, q, q2);
+    __syncthreads();
+    head_fwd<LOG_R, G::R1, G::R2, NP, false>(sm, nullptr, nullptr, rowbase,
+                                             twf, q, q2);
+    __syncthreads();
+  } else {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < G::N2; i += G::T) sm[pad(i)] = P.in0[off + i];
+    __syncthreads();
+  }
+  tail_pass<LOG_R, NP, FWD, MID, INV, MODE>(sm, rowbase, twf, twi, L, q2);
+  __syncthreads();
+  if (INV != INV_NONE || MID) {
+    head_inv<LOG_R, G::R1, G::R2, false>(sm, nullptr, rowbase, twi, L, q2,
+                                         FIN_LAZY);
+    __syncthreads();
+    head_inv<LOG_R, 0, G::R1, true>(sm, P.out + off, rowbase, twi, L, q2,
+                                    P.log_n1 == 0 ? P.fin : FIN_LAZY);
+  } else {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < G::N2; i += G::T) P.out[off + i] = sm[pad(i)];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// COLUMN kernels (N2 = 4096 columns per polynomial, N1 = 2^LOG_N1 rows)
+
+constexpr int COL_LOG_R = 12;
+constexpr int COL_THREADS = 256;
+
+struct ColParams {
+  const u64 *src0;
+  const u64 *src1;
+  u64 *dst0;
+  u64 *dst1;
+  int nsrc;  // 1 or 2 source/destination pairs
+  long long npolys;
+  TwSet tw;
+  LimbSet limbs;
+  int fin;  // inverse: FinalMode of the last stage (global m == 1)
+};
+
+template <int LOG_N1, bool INV>
+__global__ void __launch_bounds__(COL_THREADS) col_kernel(const ColParams P) {
+  constexpr int N1 = 1 << LOG_N1;
+  const long long cols = P.npolys << COL_LOG_R;
+  const long long gid = blockIdx.x * static_cast<long long>(COL_THREADS) +
+                        threadIdx.x;
+  if (gid >= cols * P.nsrc) return;
+  const int which = gid >= cols ? 1 : 0;
+  const long long rem = gid - (which ? cols : 0);
+  const long long poly = rem >> COL_LOG_R;
+  const long long base =
+      (poly << (COL_LOG_R + LOG_N1)) + (rem & ((1 << COL_LOG_R) - 1));
+  int limb;
+  const Limb L = get_limb(P.limbs, poly, limb);
+  const u64 q = L.q, q2 = 2 * L.q;
+  const u64 *__restrict__ src = (which ? P.src1 : P.src0) + base;
+  u64 *__restrict__ dst = (which ? P.dst1 : P.dst0) + base;
+  u64 x[1][N1];
+#pragma unroll
+  for (int e = 0; e < N1; ++e) x[0][e] = src[static_cast<long long>(e) << COL_LOG_R];
+  if (!INV) {
+    fwd_radix<LOG_N1, LOG_N1, 1>(x, 1, P.tw.fwd + limb * P.tw.stride, q, q2);
+  } else {
+    const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
+    inv_radix<LOG_N1, LOG_N1, 1, 1>(x, 1, twi, q, q2);
+    inv_stage0<LOG_N1, 1>(x, 1, twi, L, q2, P.fin);
+  }
+#pragma unroll
+  for (int e = 0; e < N1; ++e) dst[static_cast<long long>(e) << COL_LOG_R] = x[0][e];
+}
+
+// ---------------------------------------------------------------------------
+// SMALL kernel: n <= 2^12, one CTA per polynomial (per pair when fused);
+// stage loop over shared memory.  Used for n < 2^10 (the reference's unit
+// test sizes); also a schedule-independent cross-check of the row kernel.
+
+struct SmallParams {
+  u64 *out;
+  const u64 *in0;
+  const u64 *in1;
+  TwSet tw;
+  LimbSet limbs;
+  int log_n;
+  int fwd;  // FwdKind
+  int mid;  // fused middle (requires two inputs)
+  int inv;  // InvKind
+  int fin;  // FinalMode for the m == 1 inverse stage
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
+  extern __shared__ u64 sm[];
+  const int n = 1 << P.log_n;
+  const int np = P.mid ? 2 : 1;
+  const long long poly = blockIdx.x;
+  int limb;
+  const Limb L = get_limb(P.limbs, poly, limb);
+  const u64 q = L.q, q2 = 2 * L.q;
+  const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
+  const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
+  const long long off = poly * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sm[i] = P.in0[off + i];
+    if (np > 1) sm[n + i] = P.in1[off + i];
+  }
+  __syncthreads();
+  if (P.fwd != FWD_NONE) {
+    const int limit = (P.fwd == FWD_TRUNC) ? n / 2 : n;
+    for (int m = 1, k = n / 2; m < limit; m <<= 1, k >>= 1) {
+      for (int b = threadIdx.x; b < n / 2; b += blockDim.x) {
+        const int i = b / k, j = 2 * i * k + (b % k);
+        const ulonglong2 w = ldtw(twf, m + i);
+        for (int p = 0; p < np; ++p)
+          ct_bfly(sm[p * n + j], sm[p * n + j + k], w.x, w.y, q, q2);
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < np * n; i += blockDim.x) sm[i] = canon4(sm[i], q, q2);
+    __syncthreads();
+  }
+  if (P.mid) {
+    for (int i = threadIdx.x; i < n / 2; i += blockDim.x) {
+      const ulonglong2 w = ldtw(twf, n / 4 + i / 2);
+      u64 c0, c1;
+      fused_pair<MODE>(sm[2 * i], sm[2 * i + 1], sm[n + 2 * i], sm[n + 2 * i + 1],
+                       w.x, w.y, (i & 1) != 0, L, c0, c1);
+      sm[2 * i] = c0;
+      sm[2 * i + 1] = c1;
+    }
+    __syncthreads();
+  }
+  if (P.inv != INV_NONE) {
+    const int m0 = (P.inv == INV_SKIP) ? n / 4 : n / 2;
+    const int k0 = (P.inv == INV_SKIP) ? 2 : 1;
+    for (int m = m0, k = k0; m >= 1; m >>= 1, k <<= 1) {
+      for (int b = threadIdx.x; b < n / 2; b += blockDim.x) {
+        const int i = b / k, j = 2 * i * k + (b % k);
+        if (m == 1 && P.fin >= FIN_SCALED_FULL) {
+          const u64 *sc = (P.fin == FIN_SCALED_FULL) ? L.sc_full : L.sc_skip;
+          const u64 s[4] = {sc[0], sc[1], sc[2], sc[3]};
+          gs_bfly_last_scaled(sm[j], sm[j + k], s, q, q2);
+        } else {
+          const ulonglong2 w = ldtw(twi, m + i);
+          gs_bfly(sm[j], sm[j + k], w.x, w.y, q, q2);
+        }
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = csub(sm[i], q);
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) P.out[off + i] = sm[i];
+}
+
+// ---------------------------------------------------------------------------
+// elementwise kernels (reference _kernels.pyx hadamard / scale / fused_middle
+// / mulmod_loop)
+
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    hadamard_kernel(const u64 *__restrict__ a, const u64 *__restrict__ b,
+                    u64 *__restrict__ out, long long n, const Limb L) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * 256)
+    out[i] = mulred<MODE>(a[i], b[i], L);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    scale_kernel(u64 *__restrict__ a, u64 factor, long long n, const Limb L) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * 256)
+    a[i] = mulred<MODE>(a[i], factor, L);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    fused_middle_kernel(const u64 *__restrict__ ah, const u64 *__restrict__ bh,
+                        u64 *__restrict__ ch, const ulonglong2 *__restrict__ tw,
+                        int log_n, long long npairs, const Limb L) {
+  const int half = 1 << (log_n - 1);
+  for (long long g = blockIdx.x * 256LL + threadIdx.x; g < npairs;
+       g += static_cast<long long>(gridDim.x) * 256) {
+    const long long i = g & (half - 1);
+    const ulonglong2 w = ldtw(tw, (1LL << (log_n - 2)) + (i >> 1));
+    u64 c0, c1;
+    fused_pair<MODE>(ah[2 * g], ah[2 * g + 1], bh[2 * g], bh[2 * g + 1], w.x, w.y,
+                     (i & 1) != 0, L, c0, c1);
+    ch[2 * g] = c0;
+    ch[2 * g + 1] = c1;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    mulmod_loop_kernel(const u64 *__restrict__ a, const u64 *__restrict__ b,
+                       long long n, u64 passes, u64 *sink, const Limb L) {
+  u64 acc = 0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * 256) {
+    const u64 r = mulred<MODE>(a[i], b[i], L);
+    if (passes & 1) acc ^= r;  // x ^ x == 0: an even pass count cancels
+  }
+  for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicXor(reinterpret_cast<unsigned long long *>(sink), static_cast<unsigned long long>(acc));
+}
+
+// ---------------------------------------------------------------------------
+// plan construction (reference params.py:153-181) and validation (:184-207)
+
+__device__ __forceinline__ u64 powmod(u64 base, u64 e, const Limb &L) {
+  u64 r = 1 % L.q;
+  while (e) {
+    if (e & 1) r = mulred<NTTMUL_RED_ONE_SUB>(r, base, L);
+    base = mulred<NTTMUL_RED_ONE_SUB>(base, base, L);
+    e >>= 1;
+  }
+  return r;
+}
+
+__device__ __forceinline__ u64 shoup_companion(u64 w, u64 q) {
+  return static_cast<u64>((static_cast<unsigned __int128>(w) << 64) / q);
+}
+
+// L must carry the proposed-variant Barrett constants.
+__global__ void __launch_bounds__(256)
+    twiddle_kernel(u64 *tw_fwd, u64 *tw_inv, ulonglong2 *fwd_pairs,
+                   ulonglong2 *inv_pairs, u64 psi, u64 psi_inv, int log_n,
+                   const Limb L) {
+  const long long i = blockIdx.x * 256LL + threadIdx.x;
+  if (i >= (1LL << log_n)) return;
+  const u64 br = __brevll(static_cast<u64>(i)) >> (64 - log_n);
+  const u64 f = powmod(psi, br, L);
+  const u64 v = powmod(psi_inv, br, L);
+  if (tw_fwd) tw_fwd[i] = f;
+  if (tw_inv) tw_inv[i] = v;
+  if (fwd_pairs) fwd_pairs[i] = make_ulonglong2(f, shoup_companion(f, L.q));
+  if (inv_pairs) inv_pairs[i] = make_ulonglong2(v, shoup_companion(v, L.q));
+}
+
+__global__ void __launch_bounds__(256)
+    shoup_pairs_kernel(ulonglong2 *pairs, const u64 *tw, u64 q, long long n) {
+  const long long i = blockIdx.x * 256LL + threadIdx.x;
+  if (i < n) pairs[i] = make_ulonglong2(tw[i], shoup_companion(tw[i], q));
+}
+
+__global__ void __launch_bounds__(256)
+    check_twiddles_kernel(const u64 *f, const u64 *v, long long n,
+                          unsigned long long *bad, const Limb L) {
+  const long long i = blockIdx.x * 256LL + threadIdx.x;
+  if (i >= n) return;
+  int b = 0;
+  if (f[i] >= L.q || v[i] >= L.q ||
+      mulred<NTTMUL_RED_BUILTIN>(f[i], v[i], L) != 1)
+    b = 1;
+  if (i == 0 && (f[0] != 1 || v[0] != 1)) b += 1;
+  if (b) atomicAdd(bad, static_cast<unsigned long long>(b));
+}
+
+// ---------------------------------------------------------------------------
+// register-resident modmul microbenchmark (int-pipe roof)
+
+template <int KIND, int MODE, int CHAINS>
+__global__ void __launch_bounds__(256)
+    modmul_roof_kernel(long long iters, u64 *sink, const Limb L, u64 w,
+                       u64 wp) {
+  u64 x[CHAINS];
+  const u64 seed = (blockIdx.x * 256ULL + threadIdx.x) * 0x9E3779B97F4A7C15ULL;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) x[c] = (seed + c * 0x632BE59BD9B4E019ULL) % L.q;
+  for (long long it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) {
+      if (KIND == 0)
+        x[c] = mulred<MODE>(x[c], x[(c + 1) % CHAINS], L);
+      else
+        x[c] = shoup(x[c], w, wp, L.q);
+    }
+  }
+  u64 acc = 0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) acc ^= x[c];
+  if (acc == 0x123456789ULL) atomicXor(reinterpret_cast<unsigned long long *>(sink), static_cast<unsigned long long>(acc));  // keep the work alive
+}
+
+}  // namespace nttb

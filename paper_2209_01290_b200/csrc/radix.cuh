@@ -1,0 +1,110 @@
+// radix.cuh - register-resident multi-stage butterflies.
+//
+// The merged CT forward NTT (reference _kernels.pyx:52-85, paper Alg. 5) at
+// stage "m groups, half-size k" pairs (j, j+k) inside group i = j / 2k with
+// twiddle tw[m + i].  A thread that owns 2^R elements spaced k_last apart
+// (one "unit") can run R consecutive stages in registers: at unit-local stage
+// t the unit splits into 2^t groups and group gi uses tw[(B0 << t) + gi],
+// where B0 is the twiddle index of the unit's group at its first stage.
+// The GS inverse (reference _kernels.pyx:88-129, Alg. 6) is the exact mirror
+// with the inverse table.  Everything below is fully unrolled: element and
+// twiddle indices are compile-time, so the arrays live in registers.
+#pragma once
+#include "modarith.cuh"
+
+namespace nttb {
+
+__device__ __forceinline__ ulonglong2 ldtw(const ulonglong2 *__restrict__ tw,
+                                           u64 idx) {
+  return __ldg(tw + idx);
+}
+
+// Forward stages t in [0, TSTOP) of a radix-2^R unit, NP polynomials sharing
+// the twiddles.  Values in [0, 4q) -> [0, 4q).
+template <int R, int TSTOP, int NP>
+__device__ __forceinline__ void fwd_radix(u64 (&x)[NP][1 << R], u64 B0,
+                                          const ulonglong2 *__restrict__ tw,
+                                          u64 q, u64 q2) {
+#pragma unroll
+  for (int t = 0; t < TSTOP; ++t) {
+    const int half = 1 << (R - 1 - t);
+#pragma unroll
+    for (int gi = 0; gi < (1 << t); ++gi) {
+      const ulonglong2 w = ldtw(tw, (B0 << t) + gi);
+#pragma unroll
+      for (int e = 0; e < half; ++e) {
+        const int i0 = gi * 2 * half + e;
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+          ct_bfly(x[p][i0], x[p][i0 + half], w.x, w.y, q, q2);
+      }
+    }
+  }
+}
+
+// Inverse stages t = TSTART-1 down to TEND.  Values in [0, 2q) -> [0, 2q).
+template <int R, int TSTART, int TEND, int NP>
+__device__ __forceinline__ void inv_radix(u64 (&x)[NP][1 << R], u64 B0,
+                                          const ulonglong2 *__restrict__ tw,
+                                          u64 q, u64 q2) {
+#pragma unroll
+  for (int t = TSTART - 1; t >= TEND; --t) {
+    const int half = 1 << (R - 1 - t);
+#pragma unroll
+    for (int gi = 0; gi < (1 << t); ++gi) {
+      const ulonglong2 w = ldtw(tw, (B0 << t) + gi);
+#pragma unroll
+      for (int e = 0; e < half; ++e) {
+        const int i0 = gi * 2 * half + e;
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+          gs_bfly(x[p][i0], x[p][i0 + half], w.x, w.y, q, q2);
+      }
+    }
+  }
+}
+
+// Final-mode of the last inverse stage that a kernel runs.
+enum FinalMode {
+  FIN_LAZY = 0,         // more inverse stages follow in another pass/kernel
+  FIN_PLAIN = 1,        // global last stage, unscaled, canonical output
+  FIN_SCALED_FULL = 2,  // global last stage, x 2^-log_n (intt_gs scaled)
+  FIN_SCALED_SKIP = 3   // global last stage, x 2^-(log_n-1) (skip_first)
+};
+
+// Stage t = 0 of an inverse unit (one group, twiddle tw[B0]) with the final
+// treatment.  The scaled modes are only legal when B0 == 1 (global m == 1).
+template <int R, int NP>
+__device__ __forceinline__ void inv_stage0(u64 (&x)[NP][1 << R], u64 B0,
+                                           const ulonglong2 *__restrict__ tw,
+                                           const Limb &L, u64 q2, int fin) {
+  constexpr int half = 1 << (R - 1);
+  if (fin >= FIN_SCALED_FULL) {
+    u64 sc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      sc[i] = (fin == FIN_SCALED_FULL) ? L.sc_full[i] : L.sc_skip[i];
+#pragma unroll
+    for (int e = 0; e < half; ++e)
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+        gs_bfly_last_scaled(x[p][e], x[p][e + half], sc, L.q, q2);
+  } else {
+    const ulonglong2 w = ldtw(tw, B0);
+    if (fin == FIN_PLAIN) {
+#pragma unroll
+      for (int e = 0; e < half; ++e)
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+          gs_bfly_last_plain(x[p][e], x[p][e + half], w.x, w.y, L.q, q2);
+    } else {
+#pragma unroll
+      for (int e = 0; e < half; ++e)
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+          gs_bfly(x[p][e], x[p][e + half], w.x, w.y, L.q, q2);
+    }
+  }
+}
+
+}  // namespace nttb

@@ -1,0 +1,254 @@
+"""The kernel surface - drop-in for the reference's ``nttmul._kernels``.
+
+Same function names, argument order and in-place / accumulate semantics as
+/root/reference/pkg/src/nttmul/_kernels.pyx (what ``backend.kernels()``
+returns there), executed by the sm_100a library through the C ABI:
+
+  ntt_ct(a, tw, q, mode, mu, s_in, s_out, truncate, counts)        pyx:52-85
+  intt_gs(a, tw, q, half_q, mode, mu, s_in, s_out, scaled,
+          skip_first, counts)                                      pyx:88-129
+  fused_middle(ah, bh, ch, tw, q, mode, mu, s_in, s_out, counts)   pyx:132-177
+  hadamard(a, b, out, q, mode, mu, s_in, s_out, counts)            pyx:180-188
+  scale(a, factor, q, mode, mu, s_in, s_out, counts)               pyx:191-199
+  mulmod_loop(a, b, q, mode, mu, s_in, s_out, passes) -> int       pyx:359-371
+
+Operands may be CUDA uint64 tensors (1-D ``[n]`` as in the reference, or
+``[batch, n]`` to transform a whole batch in one launch) or numpy uint64
+arrays (staged to the device and written back in place - the host-buffer
+path).  ``counts`` (uint64[5]: modmul, addsub, half, twiddle loads,
+negations) is accumulated with the reference's closed forms, which are
+data-independent.  Launches go to torch's current stream.
+
+Not provided here: ``negacyclic_naive`` and the reduction sweeps - they are
+the reference's O(n^2)/exhaustive verification oracles, not the hot path
+(SURVEY.md §2.1); the CPU oracle in ``oracle/`` keeps them.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+
+NATIVE = True
+
+C_MODMUL, C_ADDSUB, C_HALF, C_TWIDDLE, C_NEG = range(5)
+RED_BUILTIN, RED_TWO_SUB, RED_ONE_SUB = 0, 1, 2
+
+# ---------------------------------------------------------------------------
+# twiddle pair tables: {w, floor(w 2^64 / q)} per entry, cached per table
+
+_PAIRS: dict = {}
+
+
+def _key(t: torch.Tensor, q: int):
+    return (t.data_ptr(), t.numel(), q)
+
+
+def register_pairs(tw: torch.Tensor, pairs: torch.Tensor, q: int, w1: int) -> None:
+    """Record the pair table (and tw[1]) that belongs to device table ``tw``."""
+    _PAIRS[_key(tw, q)] = (tw._version, pairs, w1, tw)
+
+
+def _pairs_for(tw, q: int):
+    """(pairs tensor, tw[1]) for a twiddle table given as tensor or ndarray."""
+    if isinstance(tw, torch.Tensor) and tw.is_cuda:
+        hit = _PAIRS.get(_key(tw, q))
+        if hit is not None and hit[0] == tw._version:
+            return hit[1], hit[2]
+        t = _device.to_device(tw)
+    else:
+        t = _device.to_device(tw)
+    pairs = torch.empty((t.numel(), 2), dtype=_device.U64, device=t.device)
+    _lib.call("nttmul_shoup_pairs", pairs.data_ptr(), t.data_ptr(), q, t.numel(),
+              _device.stream_ptr())
+    w1 = int(t[1].item()) if t.numel() > 1 else 1
+    if isinstance(tw, torch.Tensor) and tw.is_cuda:
+        register_pairs(tw, pairs, q, w1)
+    return pairs, w1
+
+
+# ---------------------------------------------------------------------------
+# operands
+
+class _Operand:
+    """A device view of an argument; numpy arguments are written back."""
+
+    __slots__ = ("host", "dev")
+
+    def __init__(self, x, name: str, writable: bool = True):
+        if isinstance(x, torch.Tensor):
+            if x.dtype != _device.U64:
+                raise ValueError(f"{name}: expected uint64, got {x.dtype}")
+            if not x.is_cuda:
+                raise ValueError(f"{name}: CPU tensors are not accepted; use a CUDA tensor "
+                                 "or a numpy array")
+            if not x.is_contiguous():
+                raise ValueError(f"{name}: tensor must be contiguous")
+            self.host, self.dev = None, x
+        elif isinstance(x, np.ndarray):
+            if x.dtype != np.uint64:
+                raise ValueError(f"{name}: Buffer dtype mismatch, expected uint64, got {x.dtype}")
+            if not x.flags.c_contiguous:
+                raise ValueError(f"{name}: ndarray is not C-contiguous")
+            if writable and not x.flags.writeable:
+                raise ValueError(f"{name}: buffer source array is read-only")
+            self.host = x
+            self.dev = torch.from_numpy(x).to(_device.device())
+        else:
+            raise TypeError(f"{name}: a bytes-like uint64 buffer or CUDA tensor is required, "
+                            f"not {type(x).__name__}")
+
+    def writeback(self) -> None:
+        if self.host is not None:
+            self.host[...] = self.dev.cpu().numpy()
+
+
+def _shape(op: _Operand) -> tuple[int, int]:
+    """(batch, n) of a [n] or [batch, n] operand."""
+    t = op.dev
+    if t.dim() == 1:
+        return 1, t.shape[0]
+    if t.dim() == 2:
+        return t.shape[0], t.shape[1]
+    raise ValueError("operands are [n] or [batch, n]")
+
+
+def _log2(n: int, what: str = "length") -> int:
+    if n < 1 or n & (n - 1):
+        raise ValueError(f"{what} {n} is not a power of two")
+    return n.bit_length() - 1
+
+
+def _add_counts(counts, vals) -> None:
+    if counts is None:
+        return
+    for i, v in enumerate(vals):
+        if v:
+            counts[i] += np.uint64(v)
+
+
+# closed-form operation counts of the reference kernels (data-independent)
+
+def _fwd_counts(n: int, truncate: bool):
+    limit = n // 2 if truncate else n
+    m, stages, groups = 1, 0, 0
+    while m < limit:
+        stages += 1
+        groups += m
+        m <<= 1
+    return (n // 2) * stages, stages, groups
+
+
+def _inv_counts(n: int, skip: bool):
+    m = n // 4 if skip else n // 2
+    stages, groups = 0, 0
+    while m >= 1:
+        stages += 1
+        groups += m
+        m >>= 1
+    return (n // 2) * stages, stages, groups
+
+
+# ---------------------------------------------------------------------------
+# the surface
+
+def ntt_ct(a, tw, q, mode, mu, s_in, s_out, truncate, counts=None):
+    """Merged CT forward NTT in place (normal -> bit-reversed order)."""
+    op = _Operand(a, "a")
+    batch, n = _shape(op)
+    log_n = _log2(n)
+    need = n // 2 if truncate else n
+    pairs, _ = _pairs_for(tw, int(q))
+    if pairs.shape[0] < max(need, 2):
+        raise ValueError(f"twiddle table has {pairs.shape[0]} entries, transform needs {need}")
+    _lib.call("nttmul_ntt_ct", op.dev.data_ptr(), pairs.data_ptr(), int(q), int(mode), int(mu),
+              int(s_in), int(s_out), int(bool(truncate)), log_n, batch, _device.stream_ptr())
+    op.writeback()
+    mul, _, groups = _fwd_counts(n, bool(truncate))
+    _add_counts(counts, (batch * mul, 2 * batch * mul, 0, batch * groups, 0))
+
+
+def intt_gs(a, tw, q, half_q, mode, mu, s_in, s_out, scaled, skip_first, counts=None):
+    """Merged GS inverse NTT in place (bit-reversed -> normal order)."""
+    op = _Operand(a, "a")
+    batch, n = _shape(op)
+    log_n = _log2(n)
+    need = n // 2 if skip_first else n
+    pairs, w1 = _pairs_for(tw, int(q))
+    if pairs.shape[0] < max(need, 2):
+        raise ValueError(f"twiddle table has {pairs.shape[0]} entries, transform needs {need}")
+    _lib.call("nttmul_intt_gs", op.dev.data_ptr(), pairs.data_ptr(), int(q), int(half_q),
+              int(mode), int(mu), int(s_in), int(s_out), int(bool(scaled)),
+              int(bool(skip_first)), log_n, batch, w1, _device.stream_ptr())
+    op.writeback()
+    mul, _, groups = _inv_counts(n, bool(skip_first))
+    _add_counts(counts, (batch * mul, 2 * batch * mul, 2 * batch * mul if scaled else 0,
+                         batch * groups, 0))
+
+
+def fused_middle(ah, bh, ch, tw, q, mode, mu, s_in, s_out, counts=None):
+    """Karatsuba-fused last-CT / pointwise / first-GS stage (Alg. 8)."""
+    oa, ob, oc = _Operand(ah, "ah", False), _Operand(bh, "bh", False), _Operand(ch, "ch")
+    batch, n = _shape(oa)
+    if _shape(ob) != (batch, n) or _shape(oc) != (batch, n):
+        raise ValueError("ah, bh, ch must share one shape")
+    log_n = _log2(n)
+    if n < 4:
+        raise ValueError("fused middle needs n >= 4")
+    pairs, _ = _pairs_for(tw, int(q))
+    _lib.call("nttmul_fused_middle", oa.dev.data_ptr(), ob.dev.data_ptr(), oc.dev.data_ptr(),
+              pairs.data_ptr(), int(q), int(mode), int(mu), int(s_in), int(s_out), log_n,
+              batch, _device.stream_ptr())
+    oc.writeback()
+    half = n // 2
+    _add_counts(counts, (4 * half * batch, 5 * half * batch, 0, half * batch,
+                         (half // 2) * batch))
+
+
+def hadamard(a, b, out, q, mode, mu, s_in, s_out, counts=None):
+    """out = a * b mod q entry-wise."""
+    oa, ob, oo = _Operand(a, "a", False), _Operand(b, "b", False), _Operand(out, "out")
+    n = oa.dev.numel()
+    if ob.dev.numel() != n or oo.dev.numel() != n:
+        raise ValueError("a, b, out must have equal length")
+    _lib.call("nttmul_hadamard", oa.dev.data_ptr(), ob.dev.data_ptr(), oo.dev.data_ptr(), n,
+              int(q), int(mode), int(mu), int(s_in), int(s_out), _device.stream_ptr())
+    oo.writeback()
+    _add_counts(counts, (n, 0, 0, 0, 0))
+
+
+def scale(a, factor, q, mode, mu, s_in, s_out, counts=None):
+    """a = a * factor mod q in place."""
+    op = _Operand(a, "a")
+    n = op.dev.numel()
+    _lib.call("nttmul_scale", op.dev.data_ptr(), int(factor), n, int(q), int(mode), int(mu),
+              int(s_in), int(s_out), _device.stream_ptr())
+    op.writeback()
+    _add_counts(counts, (n, 0, 0, 0, 0))
+
+
+def mulmod_loop(a, b, q, mode, mu, s_in, s_out, passes) -> int:
+    """XOR over ``passes`` passes of a[i]*b[i] mod q (the reference bench loop)."""
+    oa, ob = _Operand(a, "a", False), _Operand(b, "b", False)
+    n = oa.dev.numel()
+    if ob.dev.numel() != n:
+        raise ValueError("a and b must have equal length")
+    sink = torch.zeros(1, dtype=_device.U64, device=oa.dev.device)
+    _lib.call("nttmul_mulmod_loop", oa.dev.data_ptr(), ob.dev.data_ptr(), n, int(q), int(mode),
+              int(mu), int(s_in), int(s_out), int(passes), sink.data_ptr(),
+              _device.stream_ptr())
+    return int(sink.item())
+
+
+def mulmod_tensor(a, b, mod, variant: str = "proposed") -> torch.Tensor:
+    """Element-wise a*b mod q of two CUDA tensors (modarith.mulmod device path)."""
+    da, db = _device.to_device(a), _device.to_device(b)
+    if da.shape != db.shape:
+        raise ValueError(f"shape mismatch: {tuple(da.shape)} vs {tuple(db.shape)}")
+    out = torch.empty_like(da)
+    mode, mu, s_in, s_out = mod.reduction_params(variant)
+    _lib.call("nttmul_hadamard", da.data_ptr(), db.data_ptr(), out.data_ptr(), da.numel(),
+              mod.q, mode, mu, s_in, s_out, _device.stream_ptr())
+    return out
