@@ -48,6 +48,12 @@ extern "C" {
 #define NTTMUL_RED_TWO_SUB 1
 #define NTTMUL_RED_ONE_SUB 2
 
+/* OR-ed into the `mode` of the batched RNS entry points when EVERY limb's
+ * modulus is below 2^61: enables the [0, 8q) lazy-reduction bound (fewer
+ * corrections).  Without it the [0, 4q) bound valid up to 62-bit moduli is
+ * used; setting it with a 62-bit modulus gives wrong results. */
+#define NTTMUL_MODE_NARROW 0x100
+
 /* largest supported transform: n = 2^17 (BASELINE cfg4) */
 #define NTTMUL_MAX_LOG_N 17
 
@@ -177,7 +183,8 @@ int nttmul_mulmod_loop(const uint64_t *a, const uint64_t *b, int64_t n,
  * fwd_pairs / inv_pairs: device [num_limbs, n] pair tables (only the first
  * n/2 entries of each are read - the halved FusedPlan footprint,
  * polymul.py:36-55).  mode: the reduction mode every limb was prepared
- * with (one variant per basis, reference RnsBasis.build variant argument).
+ * with (one variant per basis, reference RnsBasis.build variant argument),
+ * optionally OR NTTMUL_MODE_NARROW.
  * workspace: device scratch of batch*num_limbs*n uint64, needed when
  * log_n > 12 (may alias b when b may be destroyed; never a or c).  c may
  * alias a.
@@ -205,13 +212,23 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a,
                                     uint64_t *workspace, int phases,
                                     void *stream);
 
+/*
+ * Pipeline knob of nttmul_polymul_fused_rns for n > 4096 (process-wide):
+ * the batch is processed in chunks of `chunk_waves` fused-row-kernel waves
+ * whose intermediates stay in L2 (scratch lines are discarded once read, so
+ * only a, b and c touch HBM).  chunk_waves = 0 runs the whole batch as one
+ * column / row / column sequence through HBM.  `reserved` must be >= 0.
+ */
+int nttmul_set_pipeline(int chunk_waves, int reserved);
+
 /* ---- measurement --------------------------------------------------------- */
 
 /*
  * Register-resident modmul throughput microbenchmark (the int-pipe roof):
  * every thread runs `iters` iterations of `chains` independent dependent
  * modmul chains.  kind 0 = Barrett data*data (mode from limb), 1 = Shoup
- * (fixed multiplicand).  Writes an XOR sink to *sink_out so the work cannot
+ * (fixed multiplicand), 2 = lazy forward CT butterfly, 3 = lazy inverse GS
+ * butterfly (kinds 2/3 count one modmul per butterfly; need q < 2^61).  Writes an XOR sink to *sink_out so the work cannot
  * be elided.  Returns the number of modmuls issued in *modmuls_out (host).
  */
 int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks,

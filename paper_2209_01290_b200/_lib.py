@@ -70,6 +70,7 @@ _PROTOS = {
                                           _c_i64, _c_int, _vp, _vp]),
     "nttmul_polymul_fused_rns_phases": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                                  _c_i64, _c_int, _vp, _c_int, _vp]),
+    "nttmul_set_pipeline": (_c_int, [_c_int, _c_int]),
     "nttmul_modmul_roof": (_c_int, [ctypes.POINTER(LimbStruct), _c_int, _c_int, _c_int,
                                     _c_i64, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
 }
@@ -84,7 +85,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("NTTMUL_LIB") or LIB_PATH
     if not os.path.exists(p):
         raise ImportError(
             f"{LIB_NAME} not built at {p}: run `python -c 'import __graft_entry__ as g; "

@@ -85,54 +85,55 @@ int smem_optin(K kernel, size_t bytes) {
 }
 
 // ---- row kernel dispatch ---------------------------------------------------
-template <int LOG_R, int FWD, bool MID, int INV, int MODE>
+template <int LOG_R, int FWD, bool MID, int INV, int MODE, int LB>
 int launch_row_t(const RowParams &P, long long rows, cudaStream_t st) {
   constexpr int NP = MID ? 2 : 1;
   const size_t smem = NP * RowGeom<LOG_R>::PADN * sizeof(u64);
-  auto k = row_kernel<LOG_R, FWD, MID, INV, MODE>;
+  auto k = row_kernel<LOG_R, FWD, MID, INV, MODE, LB>;
   CHECK(smem_optin(k, smem));
   k<<<static_cast<unsigned>(rows), RowGeom<LOG_R>::T, smem, st>>>(P);
   return cuda_status("row_kernel");
 }
 
-template <int FWD, bool MID, int INV, int MODE>
+template <int FWD, bool MID, int INV, int MODE, int LB>
 int launch_row_m(int log_r, const RowParams &P, long long rows, cudaStream_t st) {
   switch (log_r) {
-    case 10: return launch_row_t<10, FWD, MID, INV, MODE>(P, rows, st);
-    case 11: return launch_row_t<11, FWD, MID, INV, MODE>(P, rows, st);
-    case 12: return launch_row_t<12, FWD, MID, INV, MODE>(P, rows, st);
+    case 10: return launch_row_t<10, FWD, MID, INV, MODE, LB>(P, rows, st);
+    case 11: return launch_row_t<11, FWD, MID, INV, MODE, LB>(P, rows, st);
+    case 12: return launch_row_t<12, FWD, MID, INV, MODE, LB>(P, rows, st);
   }
   return fail(NTTMUL_EINVAL, "row size 2^%d unsupported", log_r);
 }
 
 // ---- column kernel dispatch -------------------------------------------------
-template <bool INV>
+template <bool INV, int LB>
 int launch_col(int log_n1, const ColParams &P, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(
       (P.nsrc * (P.npolys << COL_LOG_R) + COL_THREADS - 1) / COL_THREADS);
   switch (log_n1) {
-    case 1: col_kernel<1, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
-    case 2: col_kernel<2, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
-    case 3: col_kernel<3, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
-    case 4: col_kernel<4, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
-    case 5: col_kernel<5, INV><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 1: col_kernel<1, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 2: col_kernel<2, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 3: col_kernel<3, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 4: col_kernel<4, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 5: col_kernel<5, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
     default: return fail(NTTMUL_EINVAL, "column count 2^%d unsupported", log_n1);
   }
   return cuda_status("col_kernel");
 }
 
 // ---- small kernel -----------------------------------------------------------
+template <int LB>
 int launch_small(const SmallParams &P, int mode, long long npolys, cudaStream_t st) {
   const int n = 1 << P.log_n;
   const int threads = n / 2 < 32 ? 32 : (n / 2 > 256 ? 256 : n / 2);
   const size_t smem = (P.mid ? 2 : 1) * static_cast<size_t>(n) * sizeof(u64);
   switch (mode) {
-    case 0: CHECK(smem_optin(small_kernel<0>, smem));
-      small_kernel<0><<<static_cast<unsigned>(npolys), threads, smem, st>>>(P); break;
-    case 1: CHECK(smem_optin(small_kernel<1>, smem));
-      small_kernel<1><<<static_cast<unsigned>(npolys), threads, smem, st>>>(P); break;
-    default: CHECK(smem_optin(small_kernel<2>, smem));
-      small_kernel<2><<<static_cast<unsigned>(npolys), threads, smem, st>>>(P); break;
+    case 0: CHECK(smem_optin(small_kernel<0, LB>, smem));
+      small_kernel<0, LB><<<static_cast<unsigned>(npolys), threads, smem, st>>>(P); break;
+    case 1: CHECK(smem_optin(small_kernel<1, LB>, smem));
+      small_kernel<1, LB><<<static_cast<unsigned>(npolys), threads, smem, st>>>(P); break;
+    default: CHECK(smem_optin(small_kernel<2, LB>, smem));
+      small_kernel<2, LB><<<static_cast<unsigned>(npolys), threads, smem, st>>>(P); break;
   }
   return cuda_status("small_kernel");
 }
@@ -140,90 +141,149 @@ int launch_small(const SmallParams &P, int mode, long long npolys, cudaStream_t 
 constexpr int SMALL_MAX_LOG = 9;  // n <= 2^9 -> small kernel
 
 // ---- composite transforms -----------------------------------------------------
+template <int LB>
 int run_forward(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
                 long long npolys, bool truncate, cudaStream_t st) {
   if (npolys == 0) return NTTMUL_OK;
   if (log_n <= SMALL_MAX_LOG) {
     SmallParams P{a, a, nullptr, tw, ls, log_n, truncate ? FWD_TRUNC : FWD_FULL, 0,
                   INV_NONE, FIN_PLAIN};
-    return launch_small(P, NTTMUL_RED_ONE_SUB, npolys, st);
+    return launch_small<LB>(P, NTTMUL_RED_ONE_SUB, npolys, st);
   }
   const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
   const int log_n1 = log_n - log_r;
   if (log_n1 > 0) {
-    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, FIN_LAZY};
-    CHECK(launch_col<false>(log_n1, C, st));
+    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, FIN_LAZY, 0};
+    CHECK((launch_col<false, LB>(log_n1, C, st)));
   }
-  RowParams R{a, a, nullptr, tw, ls, log_n1, FIN_PLAIN};
+  RowParams R{a, a, nullptr, tw, ls, log_n1, FIN_PLAIN, 0};
   const long long rows = npolys << log_n1;
-  return truncate ? launch_row_m<FWD_TRUNC, false, INV_NONE, 2>(log_r, R, rows, st)
-                  : launch_row_m<FWD_FULL, false, INV_NONE, 2>(log_r, R, rows, st);
+  return truncate ? launch_row_m<FWD_TRUNC, false, INV_NONE, 2, LB>(log_r, R, rows, st)
+                  : launch_row_m<FWD_FULL, false, INV_NONE, 2, LB>(log_r, R, rows, st);
 }
 
+template <int LB>
 int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
                 long long npolys, bool skip, int fin, cudaStream_t st) {
   if (npolys == 0) return NTTMUL_OK;
   if (log_n <= SMALL_MAX_LOG) {
     SmallParams P{a, a, nullptr, tw, ls, log_n, FWD_NONE, 0, skip ? INV_SKIP : INV_FULL,
                   fin};
-    return launch_small(P, NTTMUL_RED_ONE_SUB, npolys, st);
+    return launch_small<LB>(P, NTTMUL_RED_ONE_SUB, npolys, st);
   }
   const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
   const int log_n1 = log_n - log_r;
-  RowParams R{a, a, nullptr, tw, ls, log_n1, fin};
+  RowParams R{a, a, nullptr, tw, ls, log_n1, fin, 0};
   const long long rows = npolys << log_n1;
-  CHECK((skip ? launch_row_m<FWD_NONE, false, INV_SKIP, 2>(log_r, R, rows, st)
-              : launch_row_m<FWD_NONE, false, INV_FULL, 2>(log_r, R, rows, st)));
+  CHECK((skip ? launch_row_m<FWD_NONE, false, INV_SKIP, 2, LB>(log_r, R, rows, st)
+              : launch_row_m<FWD_NONE, false, INV_FULL, 2, LB>(log_r, R, rows, st)));
   if (log_n1 > 0) {
-    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, fin};
-    CHECK(launch_col<true>(log_n1, C, st));
+    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, fin, 0};
+    CHECK((launch_col<true, LB>(log_n1, C, st)));
   }
   return NTTMUL_OK;
 }
 
+// Row-kernel occupancy (CTAs per SM x SMs) of one instantiation - used to
+// size pipeline chunks in whole waves.
+template <int LOG_R, int MODE, int LB>
+long long fused_rows_per_wave() {
+  static long long cached = 0;
+  if (cached) return cached;
+  int dev = 0, sms = 148, nb = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  auto k = row_kernel<LOG_R, FWD_TRUNC, true, INV_SKIP, MODE, LB>;
+  const size_t smem = 2 * RowGeom<LOG_R>::PADN * sizeof(u64);
+  smem_optin(k, smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, RowGeom<LOG_R>::T, smem) !=
+          cudaSuccess || nb < 1) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  cached = static_cast<long long>(nb) * sms;
+  return cached;
+}
+
+int g_chunk_waves = 2;  // row-kernel waves per pipeline chunk (0: no chunking)
+
+// The fused product for n > 4096 is COL -> ROW -> COL^-1.  Unchunked, the
+// intermediates round-trip HBM (a' -> c, b' -> ws).  Chunked (default), the
+// batch is cut into pieces of `g_chunk_waves` row-kernel waves; each piece
+// runs COL -> ROW -> COL^-1 on a scratch region small enough to stay in L2,
+// and its scratch lines are discarded (not written back) once consumed - so
+// HBM sees only a, b (read) and c (written).
 // phases: bit 0 = forward column pass, bit 1 = row kernel, bit 2 = inverse
 // column pass (n > 4096 only; smaller n always runs as one row kernel).
-template <int MODE>
+template <int MODE, int LB>
 int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
-                  const LimbSet &ls, int log_n, long long npolys, int phases,
+                  LimbSet ls, int log_n, long long npolys, int phases,
                   cudaStream_t st) {
   if (npolys == 0) return NTTMUL_OK;
   if (log_n <= SMALL_MAX_LOG) {
     if (!(phases & 2)) return NTTMUL_OK;
     SmallParams P{c, a, b, tw, ls, log_n, FWD_TRUNC, 1, INV_SKIP, FIN_SCALED_SKIP};
-    return launch_small(P, MODE, npolys, st);
+    return launch_small<LB>(P, MODE, npolys, st);
   }
   const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
   const int log_n1 = log_n - log_r;
-  const u64 *in0 = a, *in1 = b;
-  if (log_n1 > 0) {
+  if (log_n1 == 0) {
+    if (!(phases & 2)) return NTTMUL_OK;
+    RowParams R{c, a, b, tw, ls, 0, FIN_SCALED_SKIP, 0};
+    return launch_row_m<FWD_TRUNC, true, INV_SKIP, MODE, LB>(log_r, R, npolys, st);
+  }
+  const long long n = 1LL << log_n;
+  long long chunk = npolys;
+  if (g_chunk_waves > 0) {
+    chunk = (g_chunk_waves * fused_rows_per_wave<COL_LOG_R, MODE, LB>()) >> log_n1;
+    if (chunk < 1) chunk = 1;
+    if (2 * chunk > npolys) chunk = npolys;  // scratch must fit the workspace
+  }
+  for (long long off = 0; off < npolys; off += chunk) {
+    const long long cnt = npolys - off < chunk ? npolys - off : chunk;
+    LimbSet lc = ls;
+    lc.base = static_cast<int>((ls.base + off) % (ls.num > 0 ? ls.num : 1));
+    const bool piped = chunk < npolys;
+    u64 *sa = piped ? ws : c + off * n;              // a' (then c')
+    u64 *sb = piped ? ws + cnt * n : ws + off * n;   // b'
     if (phases & 1) {
-      ColParams C{a, b, c, ws, 2, npolys, tw, ls, FIN_LAZY};
-      CHECK(launch_col<false>(log_n1, C, st));
+      ColParams C{a + off * n, b + off * n, sa, sb, 2, cnt, tw, lc, FIN_LAZY, 0};
+      CHECK((launch_col<false, LB>(log_n1, C, st)));
     }
-    in0 = c;
-    in1 = ws;
-  }
-  if (phases & 2) {
-    RowParams R{c, in0, in1, tw, ls, log_n1, FIN_SCALED_SKIP};
-    CHECK((launch_row_m<FWD_TRUNC, true, INV_SKIP, MODE>(log_r, R, npolys << log_n1, st)));
-  }
-  if (log_n1 > 0 && (phases & 4)) {
-    ColParams C{c, nullptr, c, nullptr, 1, npolys, tw, ls, FIN_SCALED_SKIP};
-    CHECK(launch_col<true>(log_n1, C, st));
+    if (phases & 2) {
+      RowParams R{sa, sa, sb, tw, lc, log_n1, FIN_SCALED_SKIP, piped ? 1 : 0};
+      CHECK((launch_row_m<FWD_TRUNC, true, INV_SKIP, MODE, LB>(log_r, R, cnt << log_n1, st)));
+    }
+    if (phases & 4) {
+      ColParams C{sa, nullptr, c + off * n, nullptr, 1, cnt, tw, lc, FIN_SCALED_SKIP,
+                  piped ? 1 : 0};
+      CHECK((launch_col<true, LB>(log_n1, C, st)));
+    }
   }
   return NTTMUL_OK;
 }
 
-int run_polymul(int mode, u64 *c, const u64 *a, const u64 *b, u64 *ws,
+// narrow: every modulus < 2^61 -> the [0, 8q) lazy bound (LB = 8)
+int run_polymul(int mode, bool narrow, u64 *c, const u64 *a, const u64 *b, u64 *ws,
                 const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
                 int phases, cudaStream_t st) {
-  switch (mode) {
-    case 0: return run_polymul_m<0>(c, a, b, ws, tw, ls, log_n, npolys, phases, st);
-    case 1: return run_polymul_m<1>(c, a, b, ws, tw, ls, log_n, npolys, phases, st);
-    default: return run_polymul_m<2>(c, a, b, ws, tw, ls, log_n, npolys, phases, st);
+#define NTTB_PM(M, LBV) run_polymul_m<M, LBV>(c, a, b, ws, tw, ls, log_n, npolys, phases, st)
+  if (narrow) {
+    switch (mode) {
+      case 0: return NTTB_PM(0, 8);
+      case 1: return NTTB_PM(1, 8);
+      default: return NTTB_PM(2, 8);
+    }
   }
+  switch (mode) {
+    case 0: return NTTB_PM(0, 4);
+    case 1: return NTTB_PM(1, 4);
+    default: return NTTB_PM(2, 4);
+  }
+#undef NTTB_PM
 }
+
+inline bool is_narrow(u64 q) { return q < (1ULL << 61); }
 
 int check_log_n(int log_n, int min_log) {
   if (log_n < min_log || log_n > NTTMUL_MAX_LOG_N)
@@ -359,8 +419,12 @@ int nttmul_ntt_ct(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, int mode,
   LimbSet ls;
   ls.table = nullptr;
   ls.num = 1;
+  ls.base = 0;
   CHECK(single_limb(&ls.single, q, mode, mu, s_in, s_out, log_n, 1));
-  return run_forward(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0, S(stream));
+  return is_narrow(q) ? run_forward<8>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
+                                       S(stream))
+                      : run_forward<4>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
+                                       S(stream));
 }
 
 int nttmul_intt_gs(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, uint64_t half_q,
@@ -376,10 +440,13 @@ int nttmul_intt_gs(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, uint64_t h
   LimbSet ls;
   ls.table = nullptr;
   ls.num = 1;
+  ls.base = 0;
   CHECK(single_limb(&ls.single, q, mode, mu, s_in, s_out, log_n, w1_inv));
   const int fin = scaled ? (skip_first ? FIN_SCALED_SKIP : FIN_SCALED_FULL) : FIN_PLAIN;
-  return run_inverse(a, one_table(tw_pairs), ls, log_n, batch, skip_first != 0, fin,
-                     S(stream));
+  return is_narrow(q) ? run_inverse<8>(a, one_table(tw_pairs), ls, log_n, batch,
+                                       skip_first != 0, fin, S(stream))
+                      : run_inverse<4>(a, one_table(tw_pairs), ls, log_n, batch,
+                                       skip_first != 0, fin, S(stream));
 }
 
 int nttmul_fused_middle(const uint64_t *ah, const uint64_t *bh, uint64_t *ch,
@@ -483,16 +550,26 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
   }
   if (c == b && log_n > COL_LOG_R)
     return fail(NTTMUL_EINVAL, "c may not alias b");
+  const bool narrow = (mode & NTTMUL_MODE_NARROW) != 0;
+  mode &= ~NTTMUL_MODE_NARROW;
   if (mode < 0 || mode > 2) return fail(NTTMUL_EINVAL, "unknown reduction mode %d", mode);
   LimbSet ls;
   ls.table = limbs;
   ls.num = num_limbs;
+  ls.base = 0;
   std::memset(&ls.single, 0, sizeof(ls.single));
   const long long stride = 1LL << log_n;
   TwSet tw{reinterpret_cast<const ulonglong2 *>(fwd_pairs),
            reinterpret_cast<const ulonglong2 *>(inv_pairs), stride};
-  return run_polymul(mode, c, a, b, workspace, tw, ls, log_n,
+  return run_polymul(mode, narrow, c, a, b, workspace, tw, ls, log_n,
                      batch * num_limbs, phases, S(stream));
+}
+
+int nttmul_set_pipeline(int chunk_waves, int reserved) {
+  if (chunk_waves < 0 || chunk_waves > 64 || reserved < 0)
+    return fail(NTTMUL_EINVAL, "pipeline chunk_waves=%d", chunk_waves);
+  g_chunk_waves = chunk_waves;
+  return NTTMUL_OK;
 }
 
 int nttmul_polymul_fused_rns(uint64_t *c, const uint64_t *a, const uint64_t *b,
@@ -515,6 +592,14 @@ int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int
   const u64 w = (L.q >> 1) | 1, wp = shoup_host(w, L.q);
   if (kind == 1) {
     modmul_roof_kernel<1, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
+  } else if (kind == 2 || kind == 3) {
+    if (L.q >= (1ULL << 61)) return fail(NTTMUL_EINVAL, "butterfly roof needs q < 2^61");
+    if (kind == 2)
+      modmul_roof_kernel<2, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
+    else
+      modmul_roof_kernel<3, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
+    if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2);
+    return cuda_status("modmul_roof_kernel");
   } else {
     switch (L.mode) {
       case 0: modmul_roof_kernel<0, 0, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp); break;

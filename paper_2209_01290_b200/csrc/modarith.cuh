@@ -8,10 +8,8 @@
 //     runtime mode branches remain in the hot loop (mode is a template arg).
 //   * Shoup multiplication for products by a fixed twiddle (a Barrett
 //     reduction whose quotient constant floor(w * 2^64 / q) is precomputed per
-//     twiddle), used with Harvey's lazy butterflies: forward values live in
-//     [0, 4q), inverse values in [0, 2q); canonical [0, q) only at API edges.
-//     Valid for q < 2^62 (the reference's m <= 62 admissibility bound,
-//     modarith.py:57-60), which keeps 4q < 2^64.
+//     twiddle), with an approximate three-partial-product quotient, used in
+//     lazy butterflies (see LB below); canonical [0, q) only at API edges.
 // All results that leave a kernel are canonical, so they are bit-identical to
 // the reference regardless of which internal reduction produced them.
 #pragma once
@@ -29,16 +27,6 @@ typedef nttmul_limb_t Limb;
 __device__ __forceinline__ u64 csub(u64 x, u64 m) {
   const u64 t = x - m;
   return (static_cast<long long>(t) < 0) ? x : t;
-}
-
-// Shoup: x * w mod q in [0, 2q) for any 64-bit x, w < q, wp = floor(w 2^64/q).
-__device__ __forceinline__ u64 shoup_lazy(u64 x, u64 w, u64 wp, u64 q) {
-  const u64 qh = __umul64hi(x, wp);
-  return x * w - qh * q;
-}
-
-__device__ __forceinline__ u64 shoup(u64 x, u64 w, u64 wp, u64 q) {
-  return csub(shoup_lazy(x, w, wp, q), q);
 }
 
 // Barrett data x data product, a, b canonical.  MODE: NTTMUL_RED_*.
@@ -59,52 +47,146 @@ __device__ __forceinline__ u64 mulred(u64 a, u64 b, const Limb &L) {
   return r;
 }
 
-// ---- butterflies ----------------------------------------------------------
+// ---- explicit 32-bit multiply building blocks ----------------------------
+// On sm_100 every integer multiply (IMAD, IMAD.WIDE) issues to the single
+// "fmaheavy" pipe, which is the roof of this whole path.  These wrappers pin
+// the exact SASS (IMAD.WIDE.U32 / IMAD) so ptxas cannot expand a 64-bit
+// product into carry-fixup chains.
 
-// Merged CT forward butterfly (reference _kernels.pyx:66-80), Harvey lazy:
-// X, Y in [0, 4q) -> X + wY, X - wY in [0, 4q).
-__device__ __forceinline__ void ct_bfly(u64 &X, u64 &Y, u64 w, u64 wp, u64 q,
-                                        u64 q2) {
-  const u64 x = csub(X, q2);
-  const u64 t = shoup_lazy(Y, w, wp, q);
-  X = x + t;
-  Y = x - t + q2;
+__device__ __forceinline__ uint32_t lo32(u64 x) { return static_cast<uint32_t>(x); }
+__device__ __forceinline__ uint32_t hi32(u64 x) { return static_cast<uint32_t>(x >> 32); }
+
+__device__ __forceinline__ u64 mulw(uint32_t a, uint32_t b) {
+  u64 d;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(d) : "r"(a), "r"(b));
+  return d;
 }
 
-// Merged GS inverse butterfly (reference _kernels.pyx:102-118, unscaled),
-// Harvey lazy: X, Y in [0, 2q) -> X + Y, w (X - Y) in [0, 2q).
-__device__ __forceinline__ void gs_bfly(u64 &X, u64 &Y, u64 w, u64 wp, u64 q,
-                                        u64 q2) {
-  const u64 s = csub(X + Y, q2);
-  const u64 d = X - Y + q2;
-  X = s;
-  Y = shoup_lazy(d, w, wp, q);
+__device__ __forceinline__ u64 madw(uint32_t a, uint32_t b, u64 c) {
+  u64 d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+
+// Per-prime constants the butterflies need.
+struct Mod {
+  u64 q, q2, q4;
+  uint32_t nql, nqh;  // halves of 2^64 - q
+};
+
+__device__ __forceinline__ Mod make_mod(u64 q) {
+  Mod m;
+  m.q = q;
+  m.q2 = 2 * q;
+  m.q4 = 4 * q;
+  const u64 nq = 0 - q;
+  m.nql = lo32(nq);
+  m.nqh = hi32(nq);
+  return m;
+}
+
+// Shoup product x * w mod q in [0, 4q) for any x < 2^64 (w < q,
+// wp = floor(w 2^64 / q)).  The quotient uses three of the four partial
+// products of x * wp (the x_lo * wp_lo term and the low halves of the cross
+// terms are dropped): it undershoots floor(x wp / 2^64) by at most 2, so the
+// remainder lands in [0, 4q) instead of [0, 2q).  The remainder is formed as
+// x*w + qh*(2^64 - q) mod 2^64 so every step is a multiply-accumulate:
+// 5 IMAD.WIDE.U32 + 4 IMAD + one 64-bit add.
+__device__ __forceinline__ u64 shoup4(u64 x, u64 w, u64 wp, const Mod &M) {
+  const uint32_t xl = lo32(x), xh = hi32(x);
+  const u64 b = mulw(xl, hi32(wp));
+  const u64 c = mulw(xh, lo32(wp));
+  const u64 qh = madw(xh, hi32(wp), static_cast<u64>(hi32(b)) + hi32(c));
+  const uint32_t ql = lo32(qh), qhh = hi32(qh);
+  const u64 a = madw(ql, M.nql, mulw(xl, lo32(w)));
+  uint32_t h = hi32(a);
+  h = xl * hi32(w) + h;
+  h = xh * lo32(w) + h;
+  h = ql * M.nqh + h;
+  h = qhh * M.nql + h;
+  return (static_cast<u64>(h) << 32) | lo32(a);
+}
+
+// ---- butterflies ----------------------------------------------------------
+//
+// LB selects the lazy bound.  LB = 8 (every modulus < 2^61): forward values
+// live in [0, 8q), inverse values in [0, 4q) and the [0, 4q) Shoup result
+// needs no correction.  LB = 4 (moduli up to the reference's 62-bit limit,
+// modarith.py:57-60): Harvey's classic [0, 4q) / [0, 2q) with one extra
+// correction of the Shoup result.  Canonical [0, q) only at API edges, so
+// outputs are bit-identical to the reference either way.
+
+// Merged CT forward butterfly (reference _kernels.pyx:66-80).
+template <int LB>
+__device__ __forceinline__ void ct_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod &M) {
+  if (LB == 8) {
+    const u64 x = csub(X, M.q4);
+    const u64 t = shoup4(Y, w, wp, M);
+    X = x + t;
+    Y = x - t + M.q4;
+  } else {
+    const u64 x = csub(X, M.q2);
+    const u64 t = csub(shoup4(Y, w, wp, M), M.q2);
+    X = x + t;
+    Y = x - t + M.q2;
+  }
+}
+
+// Merged GS inverse butterfly (reference _kernels.pyx:102-118, unscaled).
+template <int LB>
+__device__ __forceinline__ void gs_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod &M) {
+  if (LB == 8) {
+    const u64 s = csub(X + Y, M.q4);
+    const u64 d = X - Y + M.q4;
+    X = s;
+    Y = shoup4(d, w, wp, M);
+  } else {
+    const u64 s = csub(X + Y, M.q2);
+    const u64 d = X - Y + M.q2;
+    X = s;
+    Y = csub(shoup4(d, w, wp, M), M.q2);
+  }
+}
+
+// forward-range value -> [0, q)
+template <int LB>
+__device__ __forceinline__ u64 canon_fwd(u64 x, const Mod &M) {
+  if (LB == 8) x = csub(x, M.q4);
+  return csub(csub(x, M.q2), M.q);
+}
+
+// inverse-range value -> [0, q)
+template <int LB>
+__device__ __forceinline__ u64 canon_inv(u64 x, const Mod &M) {
+  if (LB == 8) x = csub(x, M.q2);
+  return csub(x, M.q);
+}
+
+// exact canonical product by a fixed multiplier
+__device__ __forceinline__ u64 shoup(u64 x, u64 w, u64 wp, const Mod &M) {
+  return csub(csub(shoup4(x, w, wp, M), M.q2), M.q);
 }
 
 // Last GS stage (m = 1) with the scale folded in: canonical outputs.
 // sc = {f, f', tw_inv[1] f, (tw_inv[1] f)'}.  Replaces the reference's
 // per-stage halving (Zhang scaling, _kernels.pyx:115-117); the canonical
 // results are identical.
-__device__ __forceinline__ void gs_bfly_last_scaled(u64 &X, u64 &Y,
-                                                    const u64 (&sc)[4], u64 q,
-                                                    u64 q2) {
+template <int LB>
+__device__ __forceinline__ void gs_bfly_last_scaled(u64 &X, u64 &Y, const u64 (&sc)[4],
+                                                    const Mod &M) {
   const u64 s = X + Y;
-  const u64 d = X - Y + q2;
-  X = shoup(s, sc[0], sc[1], q);
-  Y = shoup(d, sc[2], sc[3], q);
+  const u64 d = X - Y + (LB == 8 ? M.q4 : M.q2);
+  X = shoup(s, sc[0], sc[1], M);
+  Y = shoup(d, sc[2], sc[3], M);
 }
 
 // Last GS stage without scaling: canonical outputs.
-__device__ __forceinline__ void gs_bfly_last_plain(u64 &X, u64 &Y, u64 w,
-                                                   u64 wp, u64 q, u64 q2) {
-  gs_bfly(X, Y, w, wp, q, q2);
-  X = csub(X, q);
-  Y = csub(Y, q);
-}
-
-// [0, 4q) -> [0, q)
-__device__ __forceinline__ u64 canon4(u64 x, u64 q, u64 q2) {
-  return csub(csub(x, q2), q);
+template <int LB>
+__device__ __forceinline__ void gs_bfly_last_plain(u64 &X, u64 &Y, u64 w, u64 wp,
+                                                   const Mod &M) {
+  gs_bfly<LB>(X, Y, w, wp, M);
+  X = canon_inv<LB>(X, M);
+  Y = canon_inv<LB>(Y, M);
 }
 
 // Karatsuba-fused middle pair (paper Alg. 8 lines 3-14, reference
@@ -114,7 +196,8 @@ __device__ __forceinline__ u64 canon4(u64 x, u64 q, u64 q2) {
 template <int MODE>
 __device__ __forceinline__ void fused_pair(u64 a0, u64 a1, u64 b0, u64 b1,
                                            u64 w, u64 wp, bool odd,
-                                           const Limb &L, u64 &c0, u64 &c1) {
+                                           const Limb &L, const Mod &M, u64 &c0,
+                                           u64 &c1) {
   const u64 q = L.q;
   const u64 u = mulred<MODE>(a0, b0, L);
   const u64 v = mulred<MODE>(a1, b1, L);
@@ -123,7 +206,7 @@ __device__ __forceinline__ void fused_pair(u64 a0, u64 a1, u64 b0, u64 b1,
   const u64 ww = mulred<MODE>(s1, s2, L);
   const u64 y = csub(ww + q - u, q);
   c1 = csub(y + q - v, q);
-  const u64 z = shoup(v, w, wp, q);
+  const u64 z = shoup(v, w, wp, M);
   c0 = odd ? csub(u + q - z, q) : csub(u + z, q);
 }
 

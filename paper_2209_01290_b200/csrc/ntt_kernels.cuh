@@ -33,16 +33,24 @@ struct LimbSet {
   const Limb *table;  // device [num] or nullptr -> use `single`
   Limb single;
   int num;
+  int base;           // polynomial index offset of this launch (chunking)
 };
 
 __device__ __forceinline__ Limb get_limb(const LimbSet &S, long long poly,
                                          int &limb) {
   if (S.table) {
-    limb = static_cast<int>(poly % S.num);
+    limb = static_cast<int>((poly + S.base) % S.num);
     return S.table[limb];
   }
   limb = 0;
   return S.single;
+}
+
+// Drop a consumed scratch line from L2 without writing it back to HBM
+// (sm_80+ discard.global.L2): intermediates of the fused pipeline live and
+// die in L2.  `line` must be 128-byte aligned and fully consumed.
+__device__ __forceinline__ void discard_line(const void *line) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
 }
 
 // padded shared-memory index: one u64 of padding per 16 keeps both the
@@ -50,21 +58,43 @@ __device__ __forceinline__ Limb get_limb(const LimbSet &S, long long poly,
 // minimum for 64-bit accesses.
 __device__ __forceinline__ int pad(int o) { return o + (o >> 4); }
 
+// resident CTAs per SM the row kernels are compiled for (register budget)
+#ifndef NTTB_ROW_MINB_FUSED
+#define NTTB_ROW_MINB_FUSED 2
+#endif
+#ifndef NTTB_ROW_MINB
+#define NTTB_ROW_MINB 2
+#endif
+
 enum FwdKind { FWD_NONE = 0, FWD_FULL = 1, FWD_TRUNC = 2 };
 enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 
 // ---------------------------------------------------------------------------
 // ROW kernel
+//
+// One CTA owns one contiguous row of N2 = 2^LOG_R coefficients (of a and b
+// when fused).  Each thread owns E = 2^LOG_E elements per pass.  The row's
+// HEAD = LOG_R - LOG_E leading stages run as register passes of <= LOG_E
+// stages over strided units (shared memory between passes); the last LOG_E
+// stages (the "tail") run on E consecutive elements, with the Karatsuba
+// middle in between when fused.  Inverse = mirror.
 
-template <int LOG_R>
+#ifndef NTTB_ROW_LOG_E
+#define NTTB_ROW_LOG_E 3
+#endif
+
+template <int LOG_R, int LOG_E = NTTB_ROW_LOG_E>
 struct RowGeom {
   static constexpr int N2 = 1 << LOG_R;
-  static constexpr int T = N2 / 16;                // threads; 16 elems each
+  static constexpr int E = 1 << LOG_E;
+  static constexpr int T = N2 / E;                 // threads per CTA
   static constexpr int PADN = N2 + N2 / 16;        // padded row length
-  static constexpr int HEAD = LOG_R - 4;           // stages before the tail
-  static constexpr int R1 = (HEAD + 1) / 2;        // first head pass
-  static constexpr int R2 = HEAD - R1;             // second head pass
-  static_assert(R1 >= 1 && R1 <= 4 && R2 >= 1 && R2 <= 4, "row size");
+  static constexpr int HEAD = LOG_R - LOG_E;       // stages before the tail
+  static constexpr int NPASS = (HEAD + LOG_E - 1) / LOG_E;
+  // stages of head pass i (balanced) and its first stage
+  __host__ __device__ static constexpr int R(int i) { return HEAD / NPASS + (i < HEAD % NPASS ? 1 : 0); }
+  __host__ __device__ static constexpr int S0(int i) { return i == 0 ? 0 : S0(i - 1) + R(i - 1); }
+  static_assert(NPASS >= 1 && NPASS <= 4, "row geometry");
 };
 
 struct RowParams {
@@ -75,133 +105,200 @@ struct RowParams {
   LimbSet limbs;
   int log_n1;  // rows per polynomial = 2^log_n1
   int fin;     // FinalMode of the global last inverse stage (if in this kernel)
+  int discard_in;  // inputs are pipeline scratch: discard their L2 lines once read
 };
 
-// forward head pass: R stages starting at row-local stage S0
-template <int LOG_R, int S0, int R, int NP, bool FROM_GLOBAL>
+// forward head pass: R stages starting at row-local stage S0.  The NP
+// polynomials are processed one after the other (the second pass over the
+// same twiddles hits L1), so only E data words per thread are live.
+template <int LB, int LOG_R, int S0, int R, int NP, bool FROM_GLOBAL>
 __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
                                          const u64 *__restrict__ g0,
                                          const u64 *__restrict__ g1,
                                          u64 rowbase,
                                          const ulonglong2 *__restrict__ tw,
-                                         u64 q, u64 q2) {
-  constexpr int T = RowGeom<LOG_R>::T;
-  constexpr int PADN = RowGeom<LOG_R>::PADN;
-  constexpr int U = 16 >> R;           // units per thread
+                                         const Mod &M) {
+  using G = RowGeom<LOG_R>;
+  constexpr int U = G::E >> R;         // units per thread
   constexpr int LK = LOG_R - S0 - R;   // log2(k_last)
+#pragma unroll 1
+  for (int p = 0; p < NP; ++p) {  // not unrolled: one polynomial's state live
+    const u64 *__restrict__ g = p == 0 ? g0 : g1;
+    u64 *__restrict__ s = sm + p * G::PADN;
 #pragma unroll
-  for (int w = 0; w < U; ++w) {
-    const int u = threadIdx.x + w * T;
-    const int g = u >> LK;
-    const int o0 = (g << (LOG_R - S0)) + (u & ((1 << LK) - 1));
-    u64 x[NP][1 << R];
+    for (int w = 0; w < U; ++w) {
+      const int u = threadIdx.x + w * G::T;
+      const int grp = u >> LK;
+      const int o0 = (grp << (LOG_R - S0)) + (u & ((1 << LK) - 1));
+#ifdef NTTB_TW_PREFETCH
+      TwBuf<0, R> twb;
+      tw_prefetch(twb, tw, (rowbase << S0) + grp);
+#endif
+      u64 x[1][1 << R];
 #pragma unroll
-    for (int e = 0; e < (1 << R); ++e) {
-      const int o = o0 + (e << LK);
-      if (FROM_GLOBAL) {
-        x[0][e] = g0[o];
-        if (NP > 1) x[NP - 1][e] = g1[o];
-      } else {
-#pragma unroll
-        for (int p = 0; p < NP; ++p) x[p][e] = sm[p * PADN + pad(o)];
+      for (int e = 0; e < (1 << R); ++e) {
+        const int o = o0 + (e << LK);
+        x[0][e] = FROM_GLOBAL ? g[o] : s[pad(o)];
       }
-    }
-    fwd_radix<R, R, NP>(x, (rowbase << S0) + g, tw, q, q2);
+#ifdef NTTB_TW_PREFETCH
+      fwd_radix_pf<LB, R, R, 1>(x, twb, M);
+#else
+      fwd_radix<LB, R, R, 1>(x, (rowbase << S0) + grp, tw, M);
+#endif
 #pragma unroll
-    for (int e = 0; e < (1 << R); ++e) {
-      const int o = o0 + (e << LK);
-#pragma unroll
-      for (int p = 0; p < NP; ++p) sm[p * PADN + pad(o)] = x[p][e];
+      for (int e = 0; e < (1 << R); ++e) s[pad(o0 + (e << LK))] = x[0][e];
     }
   }
 }
 
 // inverse head pass (mirror of head_fwd); TO_GLOBAL only for S0 == 0
-template <int LOG_R, int S0, int R, bool TO_GLOBAL>
+template <int LB, int LOG_R, int S0, int R, bool TO_GLOBAL>
 __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
                                          u64 *__restrict__ gout, u64 rowbase,
                                          const ulonglong2 *__restrict__ tw,
-                                         const Limb &L, u64 q2, int fin) {
-  constexpr int T = RowGeom<LOG_R>::T;
-  constexpr int U = 16 >> R;
+                                         const Limb &L, const Mod &M, int fin) {
+  using G = RowGeom<LOG_R>;
+  constexpr int U = G::E >> R;
   constexpr int LK = LOG_R - S0 - R;
 #pragma unroll
   for (int w = 0; w < U; ++w) {
-    const int u = threadIdx.x + w * T;
+    const int u = threadIdx.x + w * G::T;
     const int g = u >> LK;
     const int o0 = (g << (LOG_R - S0)) + (u & ((1 << LK) - 1));
+    const u64 B0 = (rowbase << S0) + g;
+#ifdef NTTB_TW_PREFETCH
+    TwBuf<0, R> twb;
+    tw_prefetch(twb, tw, B0);
+#endif
     u64 x[1][1 << R];
 #pragma unroll
     for (int e = 0; e < (1 << R); ++e) x[0][e] = sm[pad(o0 + (e << LK))];
-    const u64 B0 = (rowbase << S0) + g;
     if (TO_GLOBAL) {
-      inv_radix<R, R, 1, 1>(x, B0, tw, L.q, q2);
-      inv_stage0<R, 1>(x, B0, tw, L, q2, fin);
+#ifdef NTTB_TW_PREFETCH
+      inv_radix_pf<LB, R, R, 1, 1>(x, twb, M);
+#else
+      inv_radix<LB, R, R, 1, 1>(x, B0, tw, M);
+#endif
+      inv_stage0<LB, R, 1>(x, B0, tw, L, M, fin);
 #pragma unroll
       for (int e = 0; e < (1 << R); ++e) gout[o0 + (e << LK)] = x[0][e];
     } else {
-      inv_radix<R, R, 0, 1>(x, B0, tw, L.q, q2);
+#ifdef NTTB_TW_PREFETCH
+      inv_radix_pf<LB, R, R, 0, 1>(x, twb, M);
+#else
+      inv_radix<LB, R, R, 0, 1>(x, B0, tw, M);
+#endif
 #pragma unroll
       for (int e = 0; e < (1 << R); ++e) sm[pad(o0 + (e << LK))] = x[0][e];
     }
   }
 }
 
-// tail pass: 16 consecutive elements per thread (row-local stages
-// LOG_R-4 .. LOG_R-1), optionally with the fused middle in between.
-template <int LOG_R, int NP, int FWD, bool MID, int INV, int MODE>
-__device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
-                                          const ulonglong2 *__restrict__ twf,
-                                          const ulonglong2 *__restrict__ twi,
-                                          const Limb &L, u64 q2) {
-  constexpr int PADN = RowGeom<LOG_R>::PADN;
-  const u64 q = L.q;
-  const int o0 = threadIdx.x * 16;
-  const u64 B0 = (rowbase << (LOG_R - 4)) + threadIdx.x;
-  u64 x[NP][16];
-#pragma unroll
-  for (int e = 0; e < 16; ++e)
-#pragma unroll
-    for (int p = 0; p < NP; ++p) x[p][e] = sm[p * PADN + pad(o0 + e)];
-  if (FWD == FWD_FULL) fwd_radix<4, 4, NP>(x, B0, twf, q, q2);
-  if (FWD == FWD_TRUNC) fwd_radix<4, 3, NP>(x, B0, twf, q, q2);
-  if (MID) {
-    // pair p = (2p, 2p+1); twiddle tw[n/4 + i/2] == tw[4*B0 + p/2]; sign of
-    // the z term = parity of the global pair index = parity of p.
-    u64 c[1][16];
-#pragma unroll
-    for (int p = 0; p < 8; p += 2) {
-      const ulonglong2 w = ldtw(twf, 4 * B0 + (p >> 1));
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i0 = 2 * (p + h);
-        fused_pair<MODE>(canon4(x[0][i0], q, q2), canon4(x[0][i0 + 1], q, q2),
-                         canon4(x[NP - 1][i0], q, q2),
-                         canon4(x[NP - 1][i0 + 1], q, q2), w.x, w.y, h != 0, L,
-                         c[0][i0], c[0][i0 + 1]);
-      }
-    }
-    inv_radix<4, 3, 0, 1>(c, B0, twi, q, q2);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) sm[pad(o0 + e)] = c[0][e];
-  } else {
-    if (INV == INV_FULL) inv_radix<4, 4, 0, NP>(x, B0, twi, q, q2);
-    if (INV == INV_SKIP) inv_radix<4, 3, 0, NP>(x, B0, twi, q, q2);
-    if (INV == INV_NONE) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-#pragma unroll
-        for (int p = 0; p < NP; ++p) x[p][e] = canon4(x[p][e], q, q2);
-    }
-#pragma unroll
-    for (int e = 0; e < 16; ++e)
-#pragma unroll
-      for (int p = 0; p < NP; ++p) sm[p * PADN + pad(o0 + e)] = x[p][e];
+// all forward head passes, pass i = 0 .. NPASS-1 (pass 0 reads global)
+template <int LB, int LOG_R, int NP, int I = 0>
+__device__ __forceinline__ void head_fwd_all(u64 *sm, const u64 *g0, const u64 *g1,
+                                             u64 rowbase, const ulonglong2 *tw,
+                                             const Mod &M) {
+  using G = RowGeom<LOG_R>;
+  if constexpr (I < G::NPASS) {
+    head_fwd<LB, LOG_R, G::S0(I), G::R(I), NP, I == 0>(sm, g0, g1, rowbase, tw, M);
+    __syncthreads();
+    head_fwd_all<LB, LOG_R, NP, I + 1>(sm, g0, g1, rowbase, tw, M);
   }
 }
 
-template <int LOG_R, int FWD, bool MID, int INV, int MODE>
-__global__ void __launch_bounds__(1 << (LOG_R - 4))
+// all inverse head passes, pass i = NPASS-1 .. 0 (pass 0 writes global)
+template <int LB, int LOG_R, int I>
+__device__ __forceinline__ void head_inv_all(u64 *sm, u64 *gout, u64 rowbase,
+                                             const ulonglong2 *tw, const Limb &L,
+                                             const Mod &M, int fin) {
+  using G = RowGeom<LOG_R>;
+  if constexpr (I > 0) {
+    head_inv<LB, LOG_R, G::S0(I), G::R(I), false>(sm, nullptr, rowbase, tw, L, M,
+                                                  FIN_LAZY);
+    __syncthreads();
+    head_inv_all<LB, LOG_R, I - 1>(sm, gout, rowbase, tw, L, M, fin);
+  } else {
+    head_inv<LB, LOG_R, 0, G::R(0), true>(sm, gout, rowbase, tw, L, M, fin);
+  }
+}
+
+// tail pass: E consecutive elements per thread (the last LOG_E row-local
+// stages), optionally with the fused middle in between.
+template <int LB, int LOG_R, int NP, int FWD, bool MID, int INV, int MODE>
+__device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
+                                          const ulonglong2 *__restrict__ twf,
+                                          const ulonglong2 *__restrict__ twi,
+                                          const Limb &L, const Mod &M) {
+  using G = RowGeom<LOG_R>;
+  constexpr int E = G::E;
+  constexpr int LE = G::HEAD == 0 ? 0 : LOG_R - G::HEAD;  // = LOG_E
+  const int o0 = threadIdx.x * E;
+  const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
+#ifdef NTTB_TW_PREFETCH
+  TwBuf<0, LE - 1> twb;
+  if constexpr (MID) tw_prefetch(twb, twf, B0);
+#endif
+  u64 xa[1][E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) xa[0][e] = sm[pad(o0 + e)];
+  if constexpr (MID) {
+    // a's last truncated stages first, parked (canonical) in its own smem
+    // slots; then b's, kept in registers and overwritten by c pair by pair.
+#ifdef NTTB_TW_PREFETCH
+    fwd_radix_pf<LB, LE, LE - 1, 1>(xa, twb, M);
+#else
+    fwd_radix<LB, LE, LE - 1, 1>(xa, B0, twf, M);
+#endif
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[pad(o0 + e)] = canon_fwd<LB>(xa[0][e], M);
+#pragma unroll
+    for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + pad(o0 + e)];
+#ifdef NTTB_TW_PREFETCH
+    fwd_radix_pf<LB, LE, LE - 1, 1>(xa, twb, M);
+    tw_prefetch(twb, twi, B0);  // inverse twiddles of the same groups
+#else
+    fwd_radix<LB, LE, LE - 1, 1>(xa, B0, twf, M);
+#endif
+    // pair p = (2p, 2p+1); twiddle tw[n/4 + i/2] == tw[(B0 << (LE-2)) + p/2]
+    // (the k = 2 stage's group twiddle); sign of the z term = parity of the
+    // global pair index = parity of p.
+#pragma unroll
+    for (int p = 0; p < E / 2; p += 2) {
+      const ulonglong2 w = ldtw(twf, (B0 << (LE - 2)) + (p >> 1));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i0 = 2 * (p + h);
+        fused_pair<MODE>(sm[pad(o0 + i0)], sm[pad(o0 + i0 + 1)],
+                         canon_fwd<LB>(xa[0][i0], M), canon_fwd<LB>(xa[0][i0 + 1], M),
+                         w.x, w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
+      }
+    }
+#ifdef NTTB_TW_PREFETCH
+    inv_radix_pf<LB, LE, LE - 1, 0, 1>(xa, twb, M);
+#else
+    inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
+#endif
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[pad(o0 + e)] = xa[0][e];
+  } else {
+    static_assert(NP == 1, "unfused row passes transform one polynomial");
+    if (FWD == FWD_FULL) fwd_radix<LB, LE, LE, 1>(xa, B0, twf, M);
+    if (FWD == FWD_TRUNC) fwd_radix<LB, LE, LE - 1, 1>(xa, B0, twf, M);
+    if (INV == INV_FULL) inv_radix<LB, LE, LE, 0, 1>(xa, B0, twi, M);
+    if (INV == INV_SKIP) inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
+    if (INV == INV_NONE) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) xa[0][e] = canon_fwd<LB>(xa[0][e], M);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[pad(o0 + e)] = xa[0][e];
+  }
+}
+
+template <int LOG_R, int FWD, bool MID, int INV, int MODE, int LB>
+__global__ void __launch_bounds__(RowGeom<LOG_R>::T,
+                                  MID ? NTTB_ROW_MINB_FUSED : NTTB_ROW_MINB)
     row_kernel(const RowParams P) {
   using G = RowGeom<LOG_R>;
   constexpr int NP = MID ? 2 : 1;
@@ -211,33 +308,32 @@ __global__ void __launch_bounds__(1 << (LOG_R - 4))
   const int r = static_cast<int>(row & ((1LL << P.log_n1) - 1));
   int limb;
   const Limb L = get_limb(P.limbs, poly, limb);
-  const u64 q = L.q, q2 = 2 * L.q;
+  const Mod M = make_mod(L.q);
   const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
   const u64 rowbase = (1ULL << P.log_n1) + r;  // (N1 + r): group index base
   const long long off = row * G::N2;
 
   if (FWD != FWD_NONE) {
-    head_fwd<LOG_R, 0, G::R1, NP, true>(sm, P.in0 + off,
-                                        NP > 1 ? P.in1 + off : nullptr,
-                                        rowbase, twf, q, q2);
-    __syncthreads();
-    head_fwd<LOG_R, G::R1, G::R2, NP, false>(sm, nullptr, nullptr, rowbase,
-                                             twf, q, q2);
-    __syncthreads();
+    head_fwd_all<LB, LOG_R, NP>(sm, P.in0 + off, NP > 1 ? P.in1 + off : nullptr, rowbase,
+                                twf, M);
+    if (P.discard_in) {  // every element of the input rows is now in smem
+      constexpr int LINES = G::N2 * 8 / 128;
+      for (int i = threadIdx.x; i < NP * LINES; i += G::T) {
+        const u64 *src = (i < LINES ? P.in0 : P.in1) + off;
+        discard_line(src + (i % LINES) * 16);
+      }
+    }
   } else {
 #pragma unroll 4
     for (int i = threadIdx.x; i < G::N2; i += G::T) sm[pad(i)] = P.in0[off + i];
     __syncthreads();
   }
-  tail_pass<LOG_R, NP, FWD, MID, INV, MODE>(sm, rowbase, twf, twi, L, q2);
+  tail_pass<LB, LOG_R, NP, FWD, MID, INV, MODE>(sm, rowbase, twf, twi, L, M);
   __syncthreads();
   if (INV != INV_NONE || MID) {
-    head_inv<LOG_R, G::R1, G::R2, false>(sm, nullptr, rowbase, twi, L, q2,
-                                         FIN_LAZY);
-    __syncthreads();
-    head_inv<LOG_R, 0, G::R1, true>(sm, P.out + off, rowbase, twi, L, q2,
-                                    P.log_n1 == 0 ? P.fin : FIN_LAZY);
+    head_inv_all<LB, LOG_R, G::NPASS - 1>(sm, P.out + off, rowbase, twi, L, M,
+                                          P.log_n1 == 0 ? P.fin : FIN_LAZY);
   } else {
 #pragma unroll 4
     for (int i = threadIdx.x; i < G::N2; i += G::T) P.out[off + i] = sm[pad(i)];
@@ -260,9 +356,10 @@ struct ColParams {
   TwSet tw;
   LimbSet limbs;
   int fin;  // inverse: FinalMode of the last stage (global m == 1)
+  int discard_src;  // sources are pipeline scratch: discard after reading
 };
 
-template <int LOG_N1, bool INV>
+template <int LOG_N1, bool INV, int LB>
 __global__ void __launch_bounds__(COL_THREADS) col_kernel(const ColParams P) {
   constexpr int N1 = 1 << LOG_N1;
   const long long cols = P.npolys << COL_LOG_R;
@@ -276,18 +373,23 @@ __global__ void __launch_bounds__(COL_THREADS) col_kernel(const ColParams P) {
       (poly << (COL_LOG_R + LOG_N1)) + (rem & ((1 << COL_LOG_R) - 1));
   int limb;
   const Limb L = get_limb(P.limbs, poly, limb);
-  const u64 q = L.q, q2 = 2 * L.q;
+  const Mod M = make_mod(L.q);
   const u64 *__restrict__ src = (which ? P.src1 : P.src0) + base;
   u64 *__restrict__ dst = (which ? P.dst1 : P.dst0) + base;
   u64 x[1][N1];
 #pragma unroll
   for (int e = 0; e < N1; ++e) x[0][e] = src[static_cast<long long>(e) << COL_LOG_R];
   if (!INV) {
-    fwd_radix<LOG_N1, LOG_N1, 1>(x, 1, P.tw.fwd + limb * P.tw.stride, q, q2);
+    fwd_radix<LB, LOG_N1, LOG_N1, 1>(x, 1, P.tw.fwd + limb * P.tw.stride, M);
   } else {
     const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
-    inv_radix<LOG_N1, LOG_N1, 1, 1>(x, 1, twi, q, q2);
-    inv_stage0<LOG_N1, 1>(x, 1, twi, L, q2, P.fin);
+    inv_radix<LB, LOG_N1, LOG_N1, 1, 1>(x, 1, twi, M);
+    inv_stage0<LB, LOG_N1, 1>(x, 1, twi, L, M, P.fin);
+  }
+  if (P.discard_src && (threadIdx.x & 15) == 0) {
+    // this half-warp consumed whole 128-byte lines (16 columns x N1 rows)
+#pragma unroll
+    for (int e = 0; e < N1; ++e) discard_line(src + (static_cast<long long>(e) << COL_LOG_R));
   }
 #pragma unroll
   for (int e = 0; e < N1; ++e) dst[static_cast<long long>(e) << COL_LOG_R] = x[0][e];
@@ -311,7 +413,7 @@ struct SmallParams {
   int fin;  // FinalMode for the m == 1 inverse stage
 };
 
-template <int MODE>
+template <int MODE, int LB>
 __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
   extern __shared__ u64 sm[];
   const int n = 1 << P.log_n;
@@ -319,7 +421,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
   const long long poly = blockIdx.x;
   int limb;
   const Limb L = get_limb(P.limbs, poly, limb);
-  const u64 q = L.q, q2 = 2 * L.q;
+  const Mod M = make_mod(L.q);
   const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
   const long long off = poly * n;
@@ -335,11 +437,11 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
         const int i = b / k, j = 2 * i * k + (b % k);
         const ulonglong2 w = ldtw(twf, m + i);
         for (int p = 0; p < np; ++p)
-          ct_bfly(sm[p * n + j], sm[p * n + j + k], w.x, w.y, q, q2);
+          ct_bfly<LB>(sm[p * n + j], sm[p * n + j + k], w.x, w.y, M);
       }
       __syncthreads();
     }
-    for (int i = threadIdx.x; i < np * n; i += blockDim.x) sm[i] = canon4(sm[i], q, q2);
+    for (int i = threadIdx.x; i < np * n; i += blockDim.x) sm[i] = canon_fwd<LB>(sm[i], M);
     __syncthreads();
   }
   if (P.mid) {
@@ -347,7 +449,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
       const ulonglong2 w = ldtw(twf, n / 4 + i / 2);
       u64 c0, c1;
       fused_pair<MODE>(sm[2 * i], sm[2 * i + 1], sm[n + 2 * i], sm[n + 2 * i + 1],
-                       w.x, w.y, (i & 1) != 0, L, c0, c1);
+                       w.x, w.y, (i & 1) != 0, L, M, c0, c1);
       sm[2 * i] = c0;
       sm[2 * i + 1] = c1;
     }
@@ -362,15 +464,15 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
         if (m == 1 && P.fin >= FIN_SCALED_FULL) {
           const u64 *sc = (P.fin == FIN_SCALED_FULL) ? L.sc_full : L.sc_skip;
           const u64 s[4] = {sc[0], sc[1], sc[2], sc[3]};
-          gs_bfly_last_scaled(sm[j], sm[j + k], s, q, q2);
+          gs_bfly_last_scaled<LB>(sm[j], sm[j + k], s, M);
         } else {
           const ulonglong2 w = ldtw(twi, m + i);
-          gs_bfly(sm[j], sm[j + k], w.x, w.y, q, q2);
+          gs_bfly<LB>(sm[j], sm[j + k], w.x, w.y, M);
         }
       }
       __syncthreads();
     }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = csub(sm[i], q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = canon_inv<LB>(sm[i], M);
     __syncthreads();
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) P.out[off + i] = sm[i];
@@ -409,7 +511,7 @@ __global__ void __launch_bounds__(256)
     const ulonglong2 w = ldtw(tw, (1LL << (log_n - 2)) + (i >> 1));
     u64 c0, c1;
     fused_pair<MODE>(ah[2 * g], ah[2 * g + 1], bh[2 * g], bh[2 * g + 1], w.x, w.y,
-                     (i & 1) != 0, L, c0, c1);
+                     (i & 1) != 0, L, make_mod(L.q), c0, c1);
     ch[2 * g] = c0;
     ch[2 * g + 1] = c1;
   }
@@ -489,16 +591,25 @@ __global__ void __launch_bounds__(256)
     modmul_roof_kernel(long long iters, u64 *sink, const Limb L, u64 w,
                        u64 wp) {
   u64 x[CHAINS];
+  const Mod M = make_mod(L.q);
   const u64 seed = (blockIdx.x * 256ULL + threadIdx.x) * 0x9E3779B97F4A7C15ULL;
 #pragma unroll
   for (int c = 0; c < CHAINS; ++c) x[c] = (seed + c * 0x632BE59BD9B4E019ULL) % L.q;
   for (long long it = 0; it < iters; ++it) {
+    if (KIND == 2) {  // Harvey forward butterflies, [0, 8q) lazy bound
 #pragma unroll
-    for (int c = 0; c < CHAINS; ++c) {
-      if (KIND == 0)
-        x[c] = mulred<MODE>(x[c], x[(c + 1) % CHAINS], L);
-      else
-        x[c] = shoup(x[c], w, wp, L.q);
+      for (int c = 0; c < CHAINS / 2; ++c) ct_bfly<8>(x[c], x[c + CHAINS / 2], w, wp, M);
+    } else if (KIND == 3) {  // inverse butterflies, [0, 4q)
+#pragma unroll
+      for (int c = 0; c < CHAINS / 2; ++c) gs_bfly<8>(x[c], x[c + CHAINS / 2], w, wp, M);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) {
+        if (KIND == 0)
+          x[c] = mulred<MODE>(x[c], x[(c + 1) % CHAINS], L);
+        else
+          x[c] = shoup(x[c], w, wp, M);
+      }
     }
   }
   u64 acc = 0;

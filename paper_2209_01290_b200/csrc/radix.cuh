@@ -14,17 +14,24 @@
 
 namespace nttb {
 
+// Twiddle pair load.  NTTB_TW_LDG selects the read-only (.nc) path; the
+// default plain load keeps the compiler from hoisting every pass's twiddles
+// above the CTA barriers (which multiplies register pressure).
 __device__ __forceinline__ ulonglong2 ldtw(const ulonglong2 *__restrict__ tw,
                                            u64 idx) {
+#ifdef NTTB_TW_LDG
   return __ldg(tw + idx);
+#else
+  return tw[idx];
+#endif
 }
 
 // Forward stages t in [0, TSTOP) of a radix-2^R unit, NP polynomials sharing
-// the twiddles.  Values in [0, 4q) -> [0, 4q).
-template <int R, int TSTOP, int NP>
+// the twiddles.  Values stay in the forward lazy range of LB.
+template <int LB, int R, int TSTOP, int NP>
 __device__ __forceinline__ void fwd_radix(u64 (&x)[NP][1 << R], u64 B0,
                                           const ulonglong2 *__restrict__ tw,
-                                          u64 q, u64 q2) {
+                                          const Mod &M) {
 #pragma unroll
   for (int t = 0; t < TSTOP; ++t) {
     const int half = 1 << (R - 1 - t);
@@ -35,18 +42,17 @@ __device__ __forceinline__ void fwd_radix(u64 (&x)[NP][1 << R], u64 B0,
       for (int e = 0; e < half; ++e) {
         const int i0 = gi * 2 * half + e;
 #pragma unroll
-        for (int p = 0; p < NP; ++p)
-          ct_bfly(x[p][i0], x[p][i0 + half], w.x, w.y, q, q2);
+        for (int p = 0; p < NP; ++p) ct_bfly<LB>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
       }
     }
   }
 }
 
-// Inverse stages t = TSTART-1 down to TEND.  Values in [0, 2q) -> [0, 2q).
-template <int R, int TSTART, int TEND, int NP>
+// Inverse stages t = TSTART-1 down to TEND (inverse lazy range of LB).
+template <int LB, int R, int TSTART, int TEND, int NP>
 __device__ __forceinline__ void inv_radix(u64 (&x)[NP][1 << R], u64 B0,
                                           const ulonglong2 *__restrict__ tw,
-                                          u64 q, u64 q2) {
+                                          const Mod &M) {
 #pragma unroll
   for (int t = TSTART - 1; t >= TEND; --t) {
     const int half = 1 << (R - 1 - t);
@@ -57,8 +63,65 @@ __device__ __forceinline__ void inv_radix(u64 (&x)[NP][1 << R], u64 B0,
       for (int e = 0; e < half; ++e) {
         const int i0 = gi * 2 * half + e;
 #pragma unroll
-        for (int p = 0; p < NP; ++p)
-          gs_bfly(x[p][i0], x[p][i0 + half], w.x, w.y, q, q2);
+        for (int p = 0; p < NP; ++p) gs_bfly<LB>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+      }
+    }
+  }
+}
+
+// Twiddle prefetch: the (B0 << t) + gi pairs of stages [T0, T1) of a unit,
+// packed stage by stage (stage t at offset (1 << t) - (1 << T0)).  Issuing
+// them before the unit's data loads overlaps their L2 latency.
+template <int T0, int T1>
+struct TwBuf {
+  static constexpr int N = (1 << T1) - (1 << T0);
+  ulonglong2 w[N > 0 ? N : 1];
+};
+
+template <int T0, int T1>
+__device__ __forceinline__ void tw_prefetch(TwBuf<T0, T1> &b, const ulonglong2 *__restrict__ tw,
+                                            u64 B0) {
+#pragma unroll
+  for (int t = T0; t < T1; ++t)
+#pragma unroll
+    for (int gi = 0; gi < (1 << t); ++gi) b.w[(1 << t) - (1 << T0) + gi] = ldtw(tw, (B0 << t) + gi);
+}
+
+// fwd_radix over stages [0, TSTOP) with prefetched twiddles
+template <int LB, int R, int TSTOP, int NP>
+__device__ __forceinline__ void fwd_radix_pf(u64 (&x)[NP][1 << R], const TwBuf<0, TSTOP> &b,
+                                             const Mod &M) {
+#pragma unroll
+  for (int t = 0; t < TSTOP; ++t) {
+    const int half = 1 << (R - 1 - t);
+#pragma unroll
+    for (int gi = 0; gi < (1 << t); ++gi) {
+      const ulonglong2 w = b.w[(1 << t) - 1 + gi];
+#pragma unroll
+      for (int e = 0; e < half; ++e) {
+        const int i0 = gi * 2 * half + e;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) ct_bfly<LB>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+      }
+    }
+  }
+}
+
+// inv_radix over stages TSTART-1 .. TEND with prefetched twiddles of [0, TS)
+template <int LB, int R, int TSTART, int TEND, int NP, int TS>
+__device__ __forceinline__ void inv_radix_pf(u64 (&x)[NP][1 << R], const TwBuf<0, TS> &b,
+                                             const Mod &M) {
+#pragma unroll
+  for (int t = TSTART - 1; t >= TEND; --t) {
+    const int half = 1 << (R - 1 - t);
+#pragma unroll
+    for (int gi = 0; gi < (1 << t); ++gi) {
+      const ulonglong2 w = b.w[(1 << t) - 1 + gi];
+#pragma unroll
+      for (int e = 0; e < half; ++e) {
+        const int i0 = gi * 2 * half + e;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) gs_bfly<LB>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
       }
     }
   }
@@ -74,10 +137,10 @@ enum FinalMode {
 
 // Stage t = 0 of an inverse unit (one group, twiddle tw[B0]) with the final
 // treatment.  The scaled modes are only legal when B0 == 1 (global m == 1).
-template <int R, int NP>
+template <int LB, int R, int NP>
 __device__ __forceinline__ void inv_stage0(u64 (&x)[NP][1 << R], u64 B0,
                                            const ulonglong2 *__restrict__ tw,
-                                           const Limb &L, u64 q2, int fin) {
+                                           const Limb &L, const Mod &M, int fin) {
   constexpr int half = 1 << (R - 1);
   if (fin >= FIN_SCALED_FULL) {
     u64 sc[4];
@@ -87,8 +150,7 @@ __device__ __forceinline__ void inv_stage0(u64 (&x)[NP][1 << R], u64 B0,
 #pragma unroll
     for (int e = 0; e < half; ++e)
 #pragma unroll
-      for (int p = 0; p < NP; ++p)
-        gs_bfly_last_scaled(x[p][e], x[p][e + half], sc, L.q, q2);
+      for (int p = 0; p < NP; ++p) gs_bfly_last_scaled<LB>(x[p][e], x[p][e + half], sc, M);
   } else {
     const ulonglong2 w = ldtw(tw, B0);
     if (fin == FIN_PLAIN) {
@@ -96,13 +158,12 @@ __device__ __forceinline__ void inv_stage0(u64 (&x)[NP][1 << R], u64 B0,
       for (int e = 0; e < half; ++e)
 #pragma unroll
         for (int p = 0; p < NP; ++p)
-          gs_bfly_last_plain(x[p][e], x[p][e + half], w.x, w.y, L.q, q2);
+          gs_bfly_last_plain<LB>(x[p][e], x[p][e + half], w.x, w.y, M);
     } else {
 #pragma unroll
       for (int e = 0; e < half; ++e)
 #pragma unroll
-        for (int p = 0; p < NP; ++p)
-          gs_bfly(x[p][e], x[p][e + half], w.x, w.y, L.q, q2);
+        for (int p = 0; p < NP; ++p) gs_bfly<LB>(x[p][e], x[p][e + half], w.x, w.y, M);
     }
   }
 }

@@ -162,6 +162,14 @@ def _fused_counts(n: int, batch: int = 1) -> np.ndarray:
     return c
 
 
+MODE_NARROW = 0x100  # NTTMUL_MODE_NARROW: every modulus < 2^61 ([0, 8q) lazy bound)
+
+
+def mode_flags(mode: int, primes) -> int:
+    """Reduction mode plus NTTMUL_MODE_NARROW when all moduli are < 2^61."""
+    return mode | (MODE_NARROW if all(q < (1 << 61) for q in primes) else 0)
+
+
 def run_fused(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, fwd_pairs, inv_pairs,
               limbs_dev: torch.Tensor, log_n: int, num_limbs: int, batch: int, mode: int,
               workspace: torch.Tensor | None = None) -> None:
@@ -186,7 +194,7 @@ def polymul_fused(a, b, plan: NttPlan | FusedPlan, ctr: OpCounter | None = None)
     ta, dev_a = _coeffs(a, base.n)
     tb, dev_b = _coeffs(b, base.n)
     out = torch.empty_like(ta)
-    mode = base.red_args[1]
+    mode = mode_flags(base.red_args[1], [base.q])
     run_fused(out, ta, tb, fused.fwd_pairs_half, fused.inv_pairs_half, base.limb_device(),
               base.log_n, 1, 1, mode)
     _finish(ctr, _fused_counts(base.n))
@@ -218,6 +226,6 @@ def polymul_batch(pairs, plan: NttPlan | FusedPlan, workers: int = 1,
     A, Bm = torch.stack(cols_a), torch.stack(cols_b)
     out = torch.empty_like(A)
     run_fused(out, A, Bm, fused.fwd_pairs_half, fused.inv_pairs_half, base.limb_device(),
-              base.log_n, 1, len(pairs), base.red_args[1])
+              base.log_n, 1, len(pairs), mode_flags(base.red_args[1], [base.q]))
     _finish(ctr, _fused_counts(n, len(pairs)))
     return [_result(out[i], dev) for i in range(len(pairs))]

@@ -309,3 +309,25 @@ def test_batch_ntt_deterministic_any_workers():
     for w in (2, 8):
         out = nt.batch_ntt([r.copy() for r in rows], plan, w)
         assert all(np.array_equal(x, y.numpy()) for x, y in zip(base, out))
+
+
+@pytest.mark.parametrize("log_n,waves,B", [(16, 1, 2), (17, 1, 2), (14, 1, 3), (13, 2, 5),
+                                           (16, 0, 2)])
+def test_rns_chunked_pipeline_vs_oracle(log_n, waves, B):
+    """L2-resident chunked pipeline: chunks not aligned to ciphertexts (limb
+    offset per chunk), partial last chunk, scratch discard - all bit-exact."""
+    from paper_2209_01290_b200 import _lib
+
+    n = 1 << log_n
+    basis = nt.RnsBasis.build(n, 60, 5, seed=1)
+    A = np.stack([np.stack([rand(q, n, 31 * b + l) for l, q in enumerate(basis.primes)])
+                  for b in range(B)])
+    Bm = np.stack([np.stack([rand(q, n, 77 + 31 * b + l) for l, q in enumerate(basis.primes)])
+                   for b in range(B)])
+    want = oracle.polymul_rns(A, Bm, basis.primes, [p.psi for p in basis.plans])
+    try:
+        _lib.call("nttmul_set_pipeline", waves, 0)
+        got = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
+    finally:
+        _lib.call("nttmul_set_pipeline", 2, 0)
+    assert np.array_equal(got, want)

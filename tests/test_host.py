@@ -245,3 +245,34 @@ def test_product_path_has_no_oracle_import():
             src = open(os.path.join(pkg, f)).read()
             assert "import oracle" not in src and "from oracle" not in src, f
             assert "_kernels_py" not in src, f
+
+
+# ---- device arithmetic restated on the host (error bounds of shoup4) -------
+
+def _shoup4_host(x: int, w: int, wp: int, q: int) -> int:
+    """Bit-exact host model of modarith.cuh shoup4 (3-partial-product quotient)."""
+    M32, M64 = (1 << 32) - 1, (1 << 64) - 1
+    xl, xh, wpl, wph = x & M32, x >> 32, wp & M32, wp >> 32
+    b, c = xl * wph, xh * wpl
+    qh = (xh * wph + (b >> 32) + (c >> 32)) & M64
+    nq = (1 << 64) - q
+    a = (xl * (w & M32) + (qh & M32) * (nq & M32)) & M64
+    h = ((a >> 32) + xl * (w >> 32) + xh * (w & M32) + (qh & M32) * (nq >> 32)
+         + (qh >> 32) * (nq & M32)) & M32
+    return (h << 32) | (a & M32)
+
+
+@pytest.mark.parametrize("bits", [20, 30, 59, 60, 61, 62])
+def test_shoup4_bound_and_congruence(bits):
+    rng = random.Random(bits)
+    for _ in range(4000):
+        q = rng.randrange(1 << (bits - 1), 1 << bits) | 1
+        w = rng.randrange(q)
+        wp = (w << 64) // q
+        # inputs up to the largest lazy value the kernels feed in: 8q (q < 2^61)
+        # or 4q (62-bit moduli), plus the extremes
+        top = min((8 if bits <= 61 else 4) * q, 1 << 64)
+        for x in (0, 1, top - 1, rng.randrange(top), rng.randrange(1 << 64)):
+            r = _shoup4_host(x, w, wp, q)
+            assert r < 4 * q
+            assert r % q == x * w % q
