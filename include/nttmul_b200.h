@@ -53,6 +53,10 @@ extern "C" {
  * corrections).  Without it the [0, 4q) bound valid up to 62-bit moduli is
  * used; setting it with a 62-bit modulus gives wrong results. */
 #define NTTMUL_MODE_NARROW 0x100
+/* OR-ed in (with or without NTTMUL_MODE_NARROW) when EVERY modulus is below
+ * 2^60: the forward transform then corrects only every other stage
+ * ([0, 16q) range).  Setting it with a larger modulus gives wrong results. */
+#define NTTMUL_MODE_NARROW60 0x200
 
 /* largest supported transform: n = 2^17 (BASELINE cfg4) */
 #define NTTMUL_MAX_LOG_N 17

@@ -105,17 +105,60 @@ int launch_row_m(int log_r, const RowParams &P, long long rows, cudaStream_t st)
   return fail(NTTMUL_EINVAL, "row size 2^%d unsupported", log_r);
 }
 
+// ---- persistent fused row kernel -------------------------------------------
+#ifndef NTTB_PERSISTENT
+#define NTTB_PERSISTENT 0  // measured slower: 3 row buffers leave L1 no room for twiddles
+#endif
+template <int LOG_R, int MODE, int LB>
+int launch_row_persistent_t(const RowParams &P, long long rows, cudaStream_t st) {
+  const size_t smem = 3 * RowGeom<LOG_R>::PADN * sizeof(u64);
+  auto k = row_fused_persistent<LOG_R, MODE, LB>;
+  CHECK(smem_optin(k, smem));
+  static int slots = 0;  // resident CTAs per device for this instantiation
+  if (!slots) {
+    int dev = 0, sms = 148, nb = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, RowGeom<LOG_R>::T, smem) !=
+            cudaSuccess || nb < 1) {
+      cudaGetLastError();
+      nb = 1;
+    }
+    slots = nb * sms;
+  }
+  const long long grid = rows < slots ? rows : slots;
+  k<<<static_cast<unsigned>(grid), RowGeom<LOG_R>::T, smem, st>>>(P, rows);
+  return cuda_status("row_fused_persistent");
+}
+
+template <int MODE, int LB>
+int launch_row_fused(int log_r, const RowParams &P, long long rows, cudaStream_t st) {
+#if NTTB_PERSISTENT
+  switch (log_r) {
+    case 10: return launch_row_persistent_t<10, MODE, LB>(P, rows, st);
+    case 11: return launch_row_persistent_t<11, MODE, LB>(P, rows, st);
+    case 12: return launch_row_persistent_t<12, MODE, LB>(P, rows, st);
+  }
+  return fail(NTTMUL_EINVAL, "row size 2^%d unsupported", log_r);
+#else
+  return launch_row_m<FWD_TRUNC, true, INV_SKIP, MODE, LB>(log_r, P, rows, st);
+#endif
+}
+
 // ---- column kernel dispatch -------------------------------------------------
 template <bool INV, int LB>
 int launch_col(int log_n1, const ColParams &P, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(
-      (P.nsrc * (P.npolys << COL_LOG_R) + COL_THREADS - 1) / COL_THREADS);
+      (P.nsrc * ((P.npolys << COL_LOG_R) / COL_VEC) + COL_THREADS - 1) / COL_THREADS);
   switch (log_n1) {
     case 1: col_kernel<1, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
     case 2: col_kernel<2, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
     case 3: col_kernel<3, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
     case 4: col_kernel<4, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
     case 5: col_kernel<5, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
+#if NTTB_COL_LOG_R < 12
+    case 6: col_kernel<6, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
+#endif
     default: return fail(NTTMUL_EINVAL, "column count 2^%d unsupported", log_n1);
   }
   return cuda_status("col_kernel");
@@ -205,7 +248,7 @@ long long fused_rows_per_wave() {
   return cached;
 }
 
-int g_chunk_waves = 2;  // row-kernel waves per pipeline chunk (0: no chunking)
+int g_chunk_waves = 0;  // row-kernel waves per pipeline chunk (0: no chunking; measured slower)
 
 // The fused product for n > 4096 is COL -> ROW -> COL^-1.  Unchunked, the
 // intermediates round-trip HBM (a' -> c, b' -> ws).  Chunked (default), the
@@ -230,7 +273,7 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
   if (log_n1 == 0) {
     if (!(phases & 2)) return NTTMUL_OK;
     RowParams R{c, a, b, tw, ls, 0, FIN_SCALED_SKIP, 0};
-    return launch_row_m<FWD_TRUNC, true, INV_SKIP, MODE, LB>(log_r, R, npolys, st);
+    return launch_row_fused<MODE, LB>(log_r, R, npolys, st);
   }
   const long long n = 1LL << log_n;
   long long chunk = npolys;
@@ -252,7 +295,7 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
     }
     if (phases & 2) {
       RowParams R{sa, sa, sb, tw, lc, log_n1, FIN_SCALED_SKIP, piped ? 1 : 0};
-      CHECK((launch_row_m<FWD_TRUNC, true, INV_SKIP, MODE, LB>(log_r, R, cnt << log_n1, st)));
+      CHECK((launch_row_fused<MODE, LB>(log_r, R, cnt << log_n1, st)));
     }
     if (phases & 4) {
       ColParams C{sa, nullptr, c + off * n, nullptr, 1, cnt, tw, lc, FIN_SCALED_SKIP,
@@ -263,12 +306,20 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
   return NTTMUL_OK;
 }
 
-// narrow: every modulus < 2^61 -> the [0, 8q) lazy bound (LB = 8)
-int run_polymul(int mode, bool narrow, u64 *c, const u64 *a, const u64 *b, u64 *ws,
+// lb: lazy bound selected from the moduli (16: all < 2^60, 8: all < 2^61,
+// 4: up to 62 bits)
+int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
                 const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
                 int phases, cudaStream_t st) {
 #define NTTB_PM(M, LBV) run_polymul_m<M, LBV>(c, a, b, ws, tw, ls, log_n, npolys, phases, st)
-  if (narrow) {
+  if (lb == 16) {
+    switch (mode) {
+      case 0: return NTTB_PM(0, 16);
+      case 1: return NTTB_PM(1, 16);
+      default: return NTTB_PM(2, 16);
+    }
+  }
+  if (lb == 8) {
     switch (mode) {
       case 0: return NTTB_PM(0, 8);
       case 1: return NTTB_PM(1, 8);
@@ -283,7 +334,7 @@ int run_polymul(int mode, bool narrow, u64 *c, const u64 *a, const u64 *b, u64 *
 #undef NTTB_PM
 }
 
-inline bool is_narrow(u64 q) { return q < (1ULL << 61); }
+inline int lazy_bound(u64 q) { return q < (1ULL << 60) ? 16 : (q < (1ULL << 61) ? 8 : 4); }
 
 int check_log_n(int log_n, int min_log) {
   if (log_n < min_log || log_n > NTTMUL_MAX_LOG_N)
@@ -421,10 +472,14 @@ int nttmul_ntt_ct(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, int mode,
   ls.num = 1;
   ls.base = 0;
   CHECK(single_limb(&ls.single, q, mode, mu, s_in, s_out, log_n, 1));
-  return is_narrow(q) ? run_forward<8>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
-                                       S(stream))
-                      : run_forward<4>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
-                                       S(stream));
+  switch (lazy_bound(q)) {
+    case 16: return run_forward<16>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
+                                    S(stream));
+    case 8: return run_forward<8>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
+                                  S(stream));
+    default: return run_forward<4>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
+                                   S(stream));
+  }
 }
 
 int nttmul_intt_gs(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, uint64_t half_q,
@@ -443,10 +498,11 @@ int nttmul_intt_gs(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, uint64_t h
   ls.base = 0;
   CHECK(single_limb(&ls.single, q, mode, mu, s_in, s_out, log_n, w1_inv));
   const int fin = scaled ? (skip_first ? FIN_SCALED_SKIP : FIN_SCALED_FULL) : FIN_PLAIN;
-  return is_narrow(q) ? run_inverse<8>(a, one_table(tw_pairs), ls, log_n, batch,
-                                       skip_first != 0, fin, S(stream))
-                      : run_inverse<4>(a, one_table(tw_pairs), ls, log_n, batch,
-                                       skip_first != 0, fin, S(stream));
+  // the inverse uses the same [0, 4q) range for LB 8 and 16
+  return lazy_bound(q) >= 8 ? run_inverse<8>(a, one_table(tw_pairs), ls, log_n, batch,
+                                             skip_first != 0, fin, S(stream))
+                            : run_inverse<4>(a, one_table(tw_pairs), ls, log_n, batch,
+                                             skip_first != 0, fin, S(stream));
 }
 
 int nttmul_fused_middle(const uint64_t *ah, const uint64_t *bh, uint64_t *ch,
@@ -550,8 +606,8 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
   }
   if (c == b && log_n > COL_LOG_R)
     return fail(NTTMUL_EINVAL, "c may not alias b");
-  const bool narrow = (mode & NTTMUL_MODE_NARROW) != 0;
-  mode &= ~NTTMUL_MODE_NARROW;
+  const int lb = (mode & NTTMUL_MODE_NARROW60) ? 16 : ((mode & NTTMUL_MODE_NARROW) ? 8 : 4);
+  mode &= ~(NTTMUL_MODE_NARROW | NTTMUL_MODE_NARROW60);
   if (mode < 0 || mode > 2) return fail(NTTMUL_EINVAL, "unknown reduction mode %d", mode);
   LimbSet ls;
   ls.table = limbs;
@@ -561,7 +617,7 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
   const long long stride = 1LL << log_n;
   TwSet tw{reinterpret_cast<const ulonglong2 *>(fwd_pairs),
            reinterpret_cast<const ulonglong2 *>(inv_pairs), stride};
-  return run_polymul(mode, narrow, c, a, b, workspace, tw, ls, log_n,
+  return run_polymul(mode, lb, c, a, b, workspace, tw, ls, log_n,
                      batch * num_limbs, phases, S(stream));
 }
 
@@ -610,5 +666,16 @@ int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int
   if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * CH;
   return cuda_status("modmul_roof_kernel");
 }
+
+#ifdef NTTB_PHASE_TIMING
+// debug builds only (not in the header): copy the row-kernel phase stamps
+int nttmul_debug_phases(unsigned long long *host_out, int nrows) {
+  if (nrows > (1 << 16)) nrows = 1 << 16;
+  return cudaMemcpyFromSymbol(host_out, g_phase, sizeof(unsigned long long) * 8 * nrows) ==
+                 cudaSuccess
+             ? 0
+             : NTTMUL_ECUDA;
+}
+#endif
 
 }  // extern "C"

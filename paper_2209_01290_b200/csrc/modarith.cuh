@@ -70,7 +70,7 @@ __device__ __forceinline__ u64 madw(uint32_t a, uint32_t b, u64 c) {
 
 // Per-prime constants the butterflies need.
 struct Mod {
-  u64 q, q2, q4;
+  u64 q, q2, q4, q8;
   uint32_t nql, nqh;  // halves of 2^64 - q
 };
 
@@ -79,6 +79,7 @@ __device__ __forceinline__ Mod make_mod(u64 q) {
   m.q = q;
   m.q2 = 2 * q;
   m.q4 = 4 * q;
+  m.q8 = 8 * q;
   const u64 nq = 0 - q;
   m.nql = lo32(nq);
   m.nqh = hi32(nq);
@@ -117,9 +118,17 @@ __device__ __forceinline__ u64 shoup4(u64 x, u64 w, u64 wp, const Mod &M) {
 // outputs are bit-identical to the reference either way.
 
 // Merged CT forward butterfly (reference _kernels.pyx:66-80).
-template <int LB>
+// LB = 16 (moduli < 2^60) alternates reducing (RED) and non-reducing stages:
+// a RED stage takes X < 16q to [0, 8q) and emits < 12q, the next stage
+// skips the correction and emits < 16q - half the forward corrections.
+template <int LB, bool RED = true>
 __device__ __forceinline__ void ct_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod &M) {
-  if (LB == 8) {
+  if (LB == 16) {
+    const u64 x = RED ? csub(X, M.q8) : X;
+    const u64 t = shoup4(Y, w, wp, M);
+    X = x + t;
+    Y = x - t + M.q4;
+  } else if (LB == 8) {
     const u64 x = csub(X, M.q4);
     const u64 t = shoup4(Y, w, wp, M);
     X = x + t;
@@ -135,7 +144,7 @@ __device__ __forceinline__ void ct_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod
 // Merged GS inverse butterfly (reference _kernels.pyx:102-118, unscaled).
 template <int LB>
 __device__ __forceinline__ void gs_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod &M) {
-  if (LB == 8) {
+  if (LB >= 8) {
     const u64 s = csub(X + Y, M.q4);
     const u64 d = X - Y + M.q4;
     X = s;
@@ -151,14 +160,15 @@ __device__ __forceinline__ void gs_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod
 // forward-range value -> [0, q)
 template <int LB>
 __device__ __forceinline__ u64 canon_fwd(u64 x, const Mod &M) {
-  if (LB == 8) x = csub(x, M.q4);
+  if (LB == 16) x = csub(x, M.q8);
+  if (LB >= 8) x = csub(x, M.q4);
   return csub(csub(x, M.q2), M.q);
 }
 
 // inverse-range value -> [0, q)
 template <int LB>
 __device__ __forceinline__ u64 canon_inv(u64 x, const Mod &M) {
-  if (LB == 8) x = csub(x, M.q2);
+  if (LB >= 8) x = csub(x, M.q2);
   return csub(x, M.q);
 }
 
@@ -175,7 +185,7 @@ template <int LB>
 __device__ __forceinline__ void gs_bfly_last_scaled(u64 &X, u64 &Y, const u64 (&sc)[4],
                                                     const Mod &M) {
   const u64 s = X + Y;
-  const u64 d = X - Y + (LB == 8 ? M.q4 : M.q2);
+  const u64 d = X - Y + (LB >= 8 ? M.q4 : M.q2);
   X = shoup(s, sc[0], sc[1], M);
   Y = shoup(d, sc[2], sc[3], M);
 }

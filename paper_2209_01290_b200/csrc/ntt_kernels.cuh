@@ -36,6 +36,18 @@ struct LimbSet {
   int base;           // polynomial index offset of this launch (chunking)
 };
 
+// pointer form: fields are read where used instead of living in registers
+// for the whole kernel (the table entry stays in L1; the single-prime
+// struct lives in kernel-parameter space)
+__device__ __forceinline__ const Limb *limb_ptr(const LimbSet &S, long long poly, int &limb) {
+  if (S.table) {
+    limb = static_cast<int>((poly + S.base) % S.num);
+    return S.table + limb;
+  }
+  limb = 0;
+  return &S.single;
+}
+
 __device__ __forceinline__ Limb get_limb(const LimbSet &S, long long poly,
                                          int &limb) {
   if (S.table) {
@@ -53,10 +65,19 @@ __device__ __forceinline__ void discard_line(const void *line) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
 }
 
-// padded shared-memory index: one u64 of padding per 16 keeps both the
-// strided head passes and the 16-consecutive tail pass at the 2-wavefront
-// minimum for 64-bit accesses.
-__device__ __forceinline__ int pad(int o) { return o + (o >> 4); }
+#ifdef NTTB_PHASE_TIMING
+// debug builds only: per-CTA clock64 stamps at row-kernel phase boundaries
+__device__ unsigned long long g_phase[1 << 16][8];
+#define NTTB_STAMP(i)                                                            \
+  do {                                                                           \
+    if (threadIdx.x == 0 && blockIdx.x < (1u << 16)) g_phase[blockIdx.x][i] = clock64(); \
+  } while (0)
+#else
+#define NTTB_STAMP(i) \
+  do {                \
+  } while (0)
+#endif
+
 
 // resident CTAs per SM the row kernels are compiled for (register budget)
 #ifndef NTTB_ROW_MINB_FUSED
@@ -82,13 +103,27 @@ enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 #ifndef NTTB_ROW_LOG_E
 #define NTTB_ROW_LOG_E 3
 #endif
+#ifndef NTTB_PREFETCH_B
+#define NTTB_PREFETCH_B 1
+#endif
 
 template <int LOG_R, int LOG_E = NTTB_ROW_LOG_E>
 struct RowGeom {
   static constexpr int N2 = 1 << LOG_R;
   static constexpr int E = 1 << LOG_E;
   static constexpr int T = N2 / E;                 // threads per CTA
-  static constexpr int PADN = N2 + N2 / 16;        // padded row length
+  // shared-memory layout of a row: 4096-element rows with 8-element units use
+  // an XOR swizzle (conflict-free for every pass, no padding); other shapes
+  // pad one word per 16
+  static constexpr bool SWZ = (LOG_R == 12 && LOG_E == 3);
+  static constexpr int PADN = SWZ ? N2 : N2 + N2 / 16;
+  __device__ __forceinline__ static int idx(int o) {
+    if (SWZ) {
+      const int row = o >> 4;
+      return o ^ ((row & 7) | ((row & 4) << 1));
+    }
+    return o + (o >> 4);
+  }
   static constexpr int HEAD = LOG_R - LOG_E;       // stages before the tail
   static constexpr int NPASS = (HEAD + LOG_E - 1) / LOG_E;
   // stages of head pass i (balanced) and its first stage
@@ -138,15 +173,15 @@ __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
 #pragma unroll
       for (int e = 0; e < (1 << R); ++e) {
         const int o = o0 + (e << LK);
-        x[0][e] = FROM_GLOBAL ? g[o] : s[pad(o)];
+        x[0][e] = FROM_GLOBAL ? g[o] : s[G::idx(o)];
       }
 #ifdef NTTB_TW_PREFETCH
-      fwd_radix_pf<LB, R, R, 1>(x, twb, M);
+      fwd_radix_pf<LB, R, R, 1, S0 & 1>(x, twb, M);
 #else
-      fwd_radix<LB, R, R, 1>(x, (rowbase << S0) + grp, tw, M);
+      fwd_radix<LB, R, R, 1, S0 & 1>(x, (rowbase << S0) + grp, tw, M);
 #endif
 #pragma unroll
-      for (int e = 0; e < (1 << R); ++e) s[pad(o0 + (e << LK))] = x[0][e];
+      for (int e = 0; e < (1 << R); ++e) s[G::idx(o0 + (e << LK))] = x[0][e];
     }
   }
 }
@@ -172,7 +207,7 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
 #endif
     u64 x[1][1 << R];
 #pragma unroll
-    for (int e = 0; e < (1 << R); ++e) x[0][e] = sm[pad(o0 + (e << LK))];
+    for (int e = 0; e < (1 << R); ++e) x[0][e] = sm[G::idx(o0 + (e << LK))];
     if (TO_GLOBAL) {
 #ifdef NTTB_TW_PREFETCH
       inv_radix_pf<LB, R, R, 1, 1>(x, twb, M);
@@ -189,7 +224,7 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
       inv_radix<LB, R, R, 0, 1>(x, B0, tw, M);
 #endif
 #pragma unroll
-      for (int e = 0; e < (1 << R); ++e) sm[pad(o0 + (e << LK))] = x[0][e];
+      for (int e = 0; e < (1 << R); ++e) sm[G::idx(o0 + (e << LK))] = x[0][e];
     }
   }
 }
@@ -203,6 +238,7 @@ __device__ __forceinline__ void head_fwd_all(u64 *sm, const u64 *g0, const u64 *
   if constexpr (I < G::NPASS) {
     head_fwd<LB, LOG_R, G::S0(I), G::R(I), NP, I == 0>(sm, g0, g1, rowbase, tw, M);
     __syncthreads();
+    if (I == 0) NTTB_STAMP(1);
     head_fwd_all<LB, LOG_R, NP, I + 1>(sm, g0, g1, rowbase, tw, M);
   }
 }
@@ -220,6 +256,38 @@ __device__ __forceinline__ void head_inv_all(u64 *sm, u64 *gout, u64 rowbase,
     head_inv_all<LB, LOG_R, I - 1>(sm, gout, rowbase, tw, L, M, fin);
   } else {
     head_inv<LB, LOG_R, 0, G::R(0), true>(sm, gout, rowbase, tw, L, M, fin);
+  }
+}
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// issue the async copy of one row (N2 words) into padded smem
+template <int LOG_R>
+__device__ __forceinline__ void row_prefetch(u64 *__restrict__ dst, const u64 *__restrict__ src) {
+  using G = RowGeom<LOG_R>;
+#pragma unroll
+  for (int i = threadIdx.x; i < G::N2; i += G::T) cp_async8(dst + G::idx(i), src + i);
+}
+
+// all forward head passes of ONE polynomial already in smem `s`
+template <int LB, int LOG_R, int I = 0>
+__device__ __forceinline__ void head_fwd_all_smem(u64 *s, u64 rowbase, const ulonglong2 *tw,
+                                                  const Mod &M) {
+  using G = RowGeom<LOG_R>;
+  if constexpr (I < G::NPASS) {
+    head_fwd<LB, LOG_R, G::S0(I), G::R(I), 1, false>(s, nullptr, nullptr, rowbase, tw, M);
+    __syncthreads();
+    head_fwd_all_smem<LB, LOG_R, I + 1>(s, rowbase, tw, M);
   }
 }
 
@@ -241,24 +309,24 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
 #endif
   u64 xa[1][E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) xa[0][e] = sm[pad(o0 + e)];
+  for (int e = 0; e < E; ++e) xa[0][e] = sm[G::idx(o0 + e)];
   if constexpr (MID) {
     // a's last truncated stages first, parked (canonical) in its own smem
     // slots; then b's, kept in registers and overwritten by c pair by pair.
 #ifdef NTTB_TW_PREFETCH
-    fwd_radix_pf<LB, LE, LE - 1, 1>(xa, twb, M);
+    fwd_radix_pf<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, twb, M);
 #else
-    fwd_radix<LB, LE, LE - 1, 1>(xa, B0, twf, M);
+    fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
 #endif
 #pragma unroll
-    for (int e = 0; e < E; ++e) sm[pad(o0 + e)] = canon_fwd<LB>(xa[0][e], M);
+    for (int e = 0; e < E; ++e) sm[G::idx(o0 + e)] = canon_fwd<LB>(xa[0][e], M);
 #pragma unroll
-    for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + pad(o0 + e)];
+    for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + G::idx(o0 + e)];
 #ifdef NTTB_TW_PREFETCH
-    fwd_radix_pf<LB, LE, LE - 1, 1>(xa, twb, M);
+    fwd_radix_pf<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, twb, M);
     tw_prefetch(twb, twi, B0);  // inverse twiddles of the same groups
 #else
-    fwd_radix<LB, LE, LE - 1, 1>(xa, B0, twf, M);
+    fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
 #endif
     // pair p = (2p, 2p+1); twiddle tw[n/4 + i/2] == tw[(B0 << (LE-2)) + p/2]
     // (the k = 2 stage's group twiddle); sign of the z term = parity of the
@@ -269,7 +337,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i0 = 2 * (p + h);
-        fused_pair<MODE>(sm[pad(o0 + i0)], sm[pad(o0 + i0 + 1)],
+        fused_pair<MODE>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
                          canon_fwd<LB>(xa[0][i0], M), canon_fwd<LB>(xa[0][i0 + 1], M),
                          w.x, w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
       }
@@ -280,11 +348,11 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
     inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
 #endif
 #pragma unroll
-    for (int e = 0; e < E; ++e) sm[pad(o0 + e)] = xa[0][e];
+    for (int e = 0; e < E; ++e) sm[G::idx(o0 + e)] = xa[0][e];
   } else {
     static_assert(NP == 1, "unfused row passes transform one polynomial");
-    if (FWD == FWD_FULL) fwd_radix<LB, LE, LE, 1>(xa, B0, twf, M);
-    if (FWD == FWD_TRUNC) fwd_radix<LB, LE, LE - 1, 1>(xa, B0, twf, M);
+    if (FWD == FWD_FULL) fwd_radix<LB, LE, LE, 1, G::HEAD & 1>(xa, B0, twf, M);
+    if (FWD == FWD_TRUNC) fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
     if (INV == INV_FULL) inv_radix<LB, LE, LE, 0, 1>(xa, B0, twi, M);
     if (INV == INV_SKIP) inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
     if (INV == INV_NONE) {
@@ -292,8 +360,46 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
       for (int e = 0; e < E; ++e) xa[0][e] = canon_fwd<LB>(xa[0][e], M);
     }
 #pragma unroll
-    for (int e = 0; e < E; ++e) sm[pad(o0 + e)] = xa[0][e];
+    for (int e = 0; e < E; ++e) sm[G::idx(o0 + e)] = xa[0][e];
   }
+}
+
+// fused tail with a and b in separate smem buffers (persistent kernel);
+// c is written over a.
+template <int LB, int LOG_R, int MODE>
+__device__ __forceinline__ void tail_pass_split(u64 *__restrict__ sa, u64 *__restrict__ sb,
+                                                u64 rowbase,
+                                                const ulonglong2 *__restrict__ twf,
+                                                const ulonglong2 *__restrict__ twi,
+                                                const Limb &L, const Mod &M) {
+  using G = RowGeom<LOG_R>;
+  constexpr int E = G::E;
+  constexpr int LE = LOG_R - G::HEAD;
+  const int o0 = threadIdx.x * E;
+  const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
+  u64 xa[1][E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) xa[0][e] = sa[G::idx(o0 + e)];
+  fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
+#pragma unroll
+  for (int e = 0; e < E; ++e) sa[G::idx(o0 + e)] = canon_fwd<LB>(xa[0][e], M);
+#pragma unroll
+  for (int e = 0; e < E; ++e) xa[0][e] = sb[G::idx(o0 + e)];
+  fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
+#pragma unroll
+  for (int p = 0; p < E / 2; p += 2) {
+    const ulonglong2 w = ldtw(twf, (B0 << (LE - 2)) + (p >> 1));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i0 = 2 * (p + h);
+      fused_pair<MODE>(sa[G::idx(o0 + i0)], sa[G::idx(o0 + i0 + 1)], canon_fwd<LB>(xa[0][i0], M),
+                       canon_fwd<LB>(xa[0][i0 + 1], M), w.x, w.y, h != 0, L, M, xa[0][i0],
+                       xa[0][i0 + 1]);
+    }
+  }
+  inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
+#pragma unroll
+  for (int e = 0; e < E; ++e) sa[G::idx(o0 + e)] = xa[0][e];
 }
 
 template <int LOG_R, int FWD, bool MID, int INV, int MODE, int LB>
@@ -307,14 +413,32 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
   const long long poly = row >> P.log_n1;
   const int r = static_cast<int>(row & ((1LL << P.log_n1) - 1));
   int limb;
-  const Limb L = get_limb(P.limbs, poly, limb);
+  const Limb &L = *limb_ptr(P.limbs, poly, limb);
   const Mod M = make_mod(L.q);
   const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
   const u64 rowbase = (1ULL << P.log_n1) + r;  // (N1 + r): group index base
   const long long off = row * G::N2;
+  NTTB_STAMP(0);
 
-  if (FWD != FWD_NONE) {
+  if (MID && NTTB_PREFETCH_B) {
+    // b's row streams into its smem slot (cp.async) while a's first pass
+    // loads and transforms a; then b's first pass runs from smem.
+    row_prefetch<LOG_R>(sm + G::PADN, P.in1 + off);
+    cp_async_commit();
+    head_fwd<LB, LOG_R, 0, G::R(0), 1, true>(sm, P.in0 + off, nullptr, rowbase, twf, M);
+    cp_async_wait<0>();
+    __syncthreads();
+    NTTB_STAMP(1);
+    head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sm + G::PADN, nullptr, nullptr, rowbase, twf, M);
+    __syncthreads();
+    head_fwd_all<LB, LOG_R, NP, 1>(sm, nullptr, nullptr, rowbase, twf, M);
+    if (P.discard_in) {
+      constexpr int LINES = G::N2 * 8 / 128;
+      for (int i = threadIdx.x; i < NP * LINES; i += G::T)
+        discard_line((i < LINES ? P.in0 : P.in1) + off + (i % LINES) * 16);
+    }
+  } else if (FWD != FWD_NONE) {
     head_fwd_all<LB, LOG_R, NP>(sm, P.in0 + off, NP > 1 ? P.in1 + off : nullptr, rowbase,
                                 twf, M);
     if (P.discard_in) {  // every element of the input rows is now in smem
@@ -326,25 +450,100 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
     }
   } else {
 #pragma unroll 4
-    for (int i = threadIdx.x; i < G::N2; i += G::T) sm[pad(i)] = P.in0[off + i];
+    for (int i = threadIdx.x; i < G::N2; i += G::T) sm[G::idx(i)] = P.in0[off + i];
     __syncthreads();
   }
+  NTTB_STAMP(2);
   tail_pass<LB, LOG_R, NP, FWD, MID, INV, MODE>(sm, rowbase, twf, twi, L, M);
   __syncthreads();
+  NTTB_STAMP(3);
   if (INV != INV_NONE || MID) {
     head_inv_all<LB, LOG_R, G::NPASS - 1>(sm, P.out + off, rowbase, twi, L, M,
                                           P.log_n1 == 0 ? P.fin : FIN_LAZY);
+    __syncthreads();
+    NTTB_STAMP(4);
   } else {
 #pragma unroll 4
-    for (int i = threadIdx.x; i < G::N2; i += G::T) P.out[off + i] = sm[pad(i)];
+    for (int i = threadIdx.x; i < G::N2; i += G::T) P.out[off + i] = sm[G::idx(i)];
   }
+}
+
+// ---------------------------------------------------------------------------
+// PERSISTENT fused row kernel.  One CTA per (SM x resident slot) walks rows
+// gridDim.x apart.  Row inputs arrive by cp.async (LDGSTS) straight into
+// shared memory: b of the current row streams in while a's first pass runs,
+// and a of the NEXT row streams into a third buffer during the whole current
+// row - so the HBM latency that dominated the first pass is hidden.
+
+template <int LOG_R, int MODE, int LB>
+__global__ void __launch_bounds__(RowGeom<LOG_R>::T, NTTB_ROW_MINB_FUSED)
+    row_fused_persistent(const RowParams P, long long nrows) {
+  using G = RowGeom<LOG_R>;
+  extern __shared__ u64 smp[];
+  u64 *const bufB = smp + G::PADN;  // a alternates between smp and smp + 2 PADN
+  long long row = blockIdx.x;
+  if (row < nrows) row_prefetch<LOG_R>(smp, P.in0 + row * G::N2);
+  cp_async_commit();
+  for (int it = 0; row < nrows; row += gridDim.x, ++it) {
+    u64 *const sa = smp + ((it & 1) ? 2 * G::PADN : 0);
+    const long long poly = row >> P.log_n1;
+    const int r = static_cast<int>(row & ((1LL << P.log_n1) - 1));
+    int limb;
+    const Limb L = get_limb(P.limbs, poly, limb);
+    const Mod M = make_mod(L.q);
+    const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
+    const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
+    const u64 rowbase = (1ULL << P.log_n1) + r;
+    const long long off = row * G::N2;
+    NTTB_STAMP(0);
+    // b of this row, then a of the next row (always commit: uniform counting)
+    row_prefetch<LOG_R>(bufB, P.in1 + off);
+    cp_async_commit();
+    const long long next = row + gridDim.x;
+    if (next < nrows)
+      row_prefetch<LOG_R>(smp + ((it & 1) ? 0 : 2 * G::PADN), P.in0 + next * G::N2);
+    cp_async_commit();
+    cp_async_wait<2>();  // a(row) landed
+    __syncthreads();
+    // head passes: a from its buffer, then b once it has landed.  The two
+    // polynomials use different smem slots, so pass them separately.
+    head_fwd_all_smem<LB, LOG_R>(sa, rowbase, twf, M);
+    cp_async_wait<1>();  // b(row) landed
+    __syncthreads();
+    NTTB_STAMP(1);
+    head_fwd_all_smem<LB, LOG_R>(bufB, rowbase, twf, M);
+    if (P.discard_in) {
+      constexpr int LINES = G::N2 * 8 / 128;
+      for (int i = threadIdx.x; i < 2 * LINES; i += G::T)
+        discard_line((i < LINES ? P.in0 : P.in1) + off + (i % LINES) * 16);
+    }
+    NTTB_STAMP(2);
+    tail_pass_split<LB, LOG_R, MODE>(sa, bufB, rowbase, twf, twi, L, M);
+    __syncthreads();
+    NTTB_STAMP(3);
+    head_inv_all<LB, LOG_R, G::NPASS - 1>(sa, P.out + off, rowbase, twi, L, M,
+                                          P.log_n1 == 0 ? P.fin : FIN_LAZY);
+    __syncthreads();  // sa / bufB free before the next row's copies land there
+    NTTB_STAMP(4);
+  }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
 // COLUMN kernels (N2 = 4096 columns per polynomial, N1 = 2^LOG_N1 rows)
 
-constexpr int COL_LOG_R = 12;
+#ifndef NTTB_COL_LOG_R
+#define NTTB_COL_LOG_R 12
+#endif
+#ifndef NTTB_COL_VEC
+#define NTTB_COL_VEC 2
+#endif
+#ifndef NTTB_COL_MINB
+#define NTTB_COL_MINB 2
+#endif
+constexpr int COL_LOG_R = NTTB_COL_LOG_R;  // row length used for n > 2^COL_LOG_R
 constexpr int COL_THREADS = 256;
+constexpr int COL_VEC = NTTB_COL_VEC;      // adjacent columns per thread (1 or 2)
 
 struct ColParams {
   const u64 *src0;
@@ -359,40 +558,60 @@ struct ColParams {
   int discard_src;  // sources are pipeline scratch: discard after reading
 };
 
+// Each thread owns COL_VEC adjacent columns (one 8*COL_VEC-byte vector per
+// row, coalesced across the warp) and runs all LOG_N1 column stages on them
+// in registers; the stages' twiddles tw[1 .. N1) are uniform across the grid.
 template <int LOG_N1, bool INV, int LB>
-__global__ void __launch_bounds__(COL_THREADS) col_kernel(const ColParams P) {
+__global__ void __launch_bounds__(COL_THREADS, NTTB_COL_MINB) col_kernel(const ColParams P) {
   constexpr int N1 = 1 << LOG_N1;
-  const long long cols = P.npolys << COL_LOG_R;
+  constexpr int V = COL_VEC;
+  const long long vecs = (P.npolys << COL_LOG_R) / V;  // column vectors per source
   const long long gid = blockIdx.x * static_cast<long long>(COL_THREADS) +
                         threadIdx.x;
-  if (gid >= cols * P.nsrc) return;
-  const int which = gid >= cols ? 1 : 0;
-  const long long rem = gid - (which ? cols : 0);
+  if (gid >= vecs * P.nsrc) return;
+  const int which = gid >= vecs ? 1 : 0;
+  const long long rem = (gid - (which ? vecs : 0)) * V;  // first column (global)
   const long long poly = rem >> COL_LOG_R;
   const long long base =
       (poly << (COL_LOG_R + LOG_N1)) + (rem & ((1 << COL_LOG_R) - 1));
   int limb;
-  const Limb L = get_limb(P.limbs, poly, limb);
+  const Limb &L = *limb_ptr(P.limbs, poly, limb);
   const Mod M = make_mod(L.q);
   const u64 *__restrict__ src = (which ? P.src1 : P.src0) + base;
   u64 *__restrict__ dst = (which ? P.dst1 : P.dst0) + base;
-  u64 x[1][N1];
+  u64 x[V][N1];
 #pragma unroll
-  for (int e = 0; e < N1; ++e) x[0][e] = src[static_cast<long long>(e) << COL_LOG_R];
+  for (int e = 0; e < N1; ++e) {
+    const long long o = static_cast<long long>(e) << COL_LOG_R;
+    if (V == 2) {
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(src + o);
+      x[0][e] = v.x;
+      x[V - 1][e] = v.y;
+    } else {
+      x[0][e] = src[o];
+    }
+  }
   if (!INV) {
-    fwd_radix<LB, LOG_N1, LOG_N1, 1>(x, 1, P.tw.fwd + limb * P.tw.stride, M);
+    fwd_radix<LB, LOG_N1, LOG_N1, V>(x, 1, P.tw.fwd + limb * P.tw.stride, M);
   } else {
     const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
-    inv_radix<LB, LOG_N1, LOG_N1, 1, 1>(x, 1, twi, M);
-    inv_stage0<LB, LOG_N1, 1>(x, 1, twi, L, M, P.fin);
+    inv_radix<LB, LOG_N1, LOG_N1, 1, V>(x, 1, twi, M);
+    inv_stage0<LB, LOG_N1, V>(x, 1, twi, L, M, P.fin);
   }
-  if (P.discard_src && (threadIdx.x & 15) == 0) {
-    // this half-warp consumed whole 128-byte lines (16 columns x N1 rows)
+  if (P.discard_src && (threadIdx.x & (16 / V - 1)) == 0) {
+    // these 16/V lanes consumed whole 128-byte lines (16 columns x N1 rows)
 #pragma unroll
     for (int e = 0; e < N1; ++e) discard_line(src + (static_cast<long long>(e) << COL_LOG_R));
   }
 #pragma unroll
-  for (int e = 0; e < N1; ++e) dst[static_cast<long long>(e) << COL_LOG_R] = x[0][e];
+  for (int e = 0; e < N1; ++e) {
+    const long long o = static_cast<long long>(e) << COL_LOG_R;
+    if (V == 2) {
+      *reinterpret_cast<ulonglong2 *>(dst + o) = make_ulonglong2(x[0][e], x[V - 1][e]);
+    } else {
+      dst[o] = x[0][e];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -432,12 +651,15 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
   __syncthreads();
   if (P.fwd != FWD_NONE) {
     const int limit = (P.fwd == FWD_TRUNC) ? n / 2 : n;
-    for (int m = 1, k = n / 2; m < limit; m <<= 1, k >>= 1) {
+    for (int m = 1, k = n / 2, stage = 0; m < limit; m <<= 1, k >>= 1, ++stage) {
       for (int b = threadIdx.x; b < n / 2; b += blockDim.x) {
         const int i = b / k, j = 2 * i * k + (b % k);
         const ulonglong2 w = ldtw(twf, m + i);
         for (int p = 0; p < np; ++p)
-          ct_bfly<LB>(sm[p * n + j], sm[p * n + j + k], w.x, w.y, M);
+          if (LB != 16 || (stage & 1) == 0)
+            ct_bfly<LB, true>(sm[p * n + j], sm[p * n + j + k], w.x, w.y, M);
+          else
+            ct_bfly<LB, false>(sm[p * n + j], sm[p * n + j + k], w.x, w.y, M);
       }
       __syncthreads();
     }

@@ -28,7 +28,9 @@ __device__ __forceinline__ ulonglong2 ldtw(const ulonglong2 *__restrict__ tw,
 
 // Forward stages t in [0, TSTOP) of a radix-2^R unit, NP polynomials sharing
 // the twiddles.  Values stay in the forward lazy range of LB.
-template <int LB, int R, int TSTOP, int NP>
+// PAR: parity of the kernel-local index of stage t = 0 (LB = 16 reduces on
+// even kernel-local stages, so every kernel starts with a reducing stage).
+template <int LB, int R, int TSTOP, int NP, int PAR = 0>
 __device__ __forceinline__ void fwd_radix(u64 (&x)[NP][1 << R], u64 B0,
                                           const ulonglong2 *__restrict__ tw,
                                           const Mod &M) {
@@ -42,7 +44,12 @@ __device__ __forceinline__ void fwd_radix(u64 (&x)[NP][1 << R], u64 B0,
       for (int e = 0; e < half; ++e) {
         const int i0 = gi * 2 * half + e;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) ct_bfly<LB>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+        for (int p = 0; p < NP; ++p) {
+          if (((PAR + t) & 1) == 0)
+            ct_bfly<LB, true>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+          else
+            ct_bfly<LB, false>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+        }
       }
     }
   }
@@ -88,7 +95,7 @@ __device__ __forceinline__ void tw_prefetch(TwBuf<T0, T1> &b, const ulonglong2 *
 }
 
 // fwd_radix over stages [0, TSTOP) with prefetched twiddles
-template <int LB, int R, int TSTOP, int NP>
+template <int LB, int R, int TSTOP, int NP, int PAR = 0>
 __device__ __forceinline__ void fwd_radix_pf(u64 (&x)[NP][1 << R], const TwBuf<0, TSTOP> &b,
                                              const Mod &M) {
 #pragma unroll
@@ -101,7 +108,12 @@ __device__ __forceinline__ void fwd_radix_pf(u64 (&x)[NP][1 << R], const TwBuf<0
       for (int e = 0; e < half; ++e) {
         const int i0 = gi * 2 * half + e;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) ct_bfly<LB>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+        for (int p = 0; p < NP; ++p) {
+          if (((PAR + t) & 1) == 0)
+            ct_bfly<LB, true>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+          else
+            ct_bfly<LB, false>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+        }
       }
     }
   }

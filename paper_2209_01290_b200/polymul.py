@@ -162,19 +162,23 @@ def _fused_counts(n: int, batch: int = 1) -> np.ndarray:
     return c
 
 
-MODE_NARROW = 0x100  # NTTMUL_MODE_NARROW: every modulus < 2^61 ([0, 8q) lazy bound)
+MODE_NARROW = 0x100    # NTTMUL_MODE_NARROW: every modulus < 2^61 ([0, 8q) lazy bound)
+MODE_NARROW60 = 0x200  # NTTMUL_MODE_NARROW60: every modulus < 2^60 ([0, 16q) forward)
 
 
 def mode_flags(mode: int, primes) -> int:
-    """Reduction mode plus NTTMUL_MODE_NARROW when all moduli are < 2^61."""
-    return mode | (MODE_NARROW if all(q < (1 << 61) for q in primes) else 0)
+    """Reduction mode plus the lazy-bound flags the moduli allow."""
+    top = max(primes)
+    if top < (1 << 60):
+        return mode | MODE_NARROW | MODE_NARROW60
+    return mode | (MODE_NARROW if top < (1 << 61) else 0)
 
 
 def run_fused(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, fwd_pairs, inv_pairs,
               limbs_dev: torch.Tensor, log_n: int, num_limbs: int, batch: int, mode: int,
               workspace: torch.Tensor | None = None) -> None:
     """Launch the fused RNS polymul over [batch, num_limbs, n] device tensors."""
-    if log_n > 12 and workspace is None:
+    if log_n > 10 and workspace is None:  # column passes need scratch (n > row length)
         workspace = torch.empty_like(a)
     _lib.call("nttmul_polymul_fused_rns", out.data_ptr(), a.data_ptr(), b.data_ptr(),
               limbs_dev.data_ptr(), fwd_pairs.data_ptr(), inv_pairs.data_ptr(), log_n,

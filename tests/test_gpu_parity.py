@@ -329,5 +329,5 @@ def test_rns_chunked_pipeline_vs_oracle(log_n, waves, B):
         _lib.call("nttmul_set_pipeline", waves, 0)
         got = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
     finally:
-        _lib.call("nttmul_set_pipeline", 2, 0)
+        _lib.call("nttmul_set_pipeline", 0, 0)
     assert np.array_equal(got, want)
