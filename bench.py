@@ -172,8 +172,9 @@ def cpu_reference_rate(basis_primes, psis, n, A, B, seconds: float, threads: int
             list(pool.map(span, spans))
         return time.perf_counter() - t0, outs
 
-    dt1, outs = run(1)
-    nct = max(1, int(seconds / max(dt1, 1e-3)))
+    ncal = max(1, -(-threads // L))  # enough items to occupy every thread once
+    dt1, outs = run(ncal)
+    nct = max(1, int(seconds * ncal / max(dt1, 1e-3)))
     dt, _ = run(nct)
     rate = nct / dt
     sample = (f"{nct} ciphertext(s) x {L} limbs of N={n} via "
@@ -273,7 +274,7 @@ def main():
     row_ms = phase_ms["row_fused"]
     row_rate = products_per_step * row_kernel_modmuls(n) / (row_ms / 1e3) / 1e9
     all_rate = products_per_step * modmuls_per_product(n) / (ms_per_step / 1e3) / 1e9
-    traffic = load_traffic("row_fused")
+    traffic = load_traffic("row_fused", products_per_step)
     roofline = {
         "bound": "int", "kernel": "row_fused (fwd row stages a,b + Karatsuba middle + inv row stages)",
         "achieved": round(row_rate, 2), "peak": round(roof["peak"], 2), "unit": "Gmodmul/s",
@@ -408,13 +409,18 @@ def peak_hbm():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def load_traffic(kernel: str):
+def load_traffic(kernel: str, products: int):
+    """DRAM bytes per launch of `kernel` at this batch, from the committed ncu
+    capture (profiles/traffic.json, bytes per limb-product), or None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(kernel)
+            rec = json.load(fh).get(kernel)
     except (OSError, ValueError):
         return None
+    if not rec:
+        return None
+    return int(rec["bytes_per_product"] * products)
 
 
 def ntt_latency_us(nt, plan):

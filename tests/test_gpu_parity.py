@@ -331,3 +331,34 @@ def test_rns_chunked_pipeline_vs_oracle(log_n, waves, B):
     finally:
         _lib.call("nttmul_set_pipeline", 0, 0)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("bits", [24, 30, 59, 60, 61, 62])
+@pytest.mark.parametrize("log_n", [10, 13, 16])
+def test_lazy_bound_paths_vs_oracle(bits, log_n):
+    """Every lazy-reduction regime: [0,16q) forward (q < 2^60), [0,8q)
+    (q < 2^61) and Harvey [0,4q) (62-bit) through the fused RNS path and the
+    standalone transforms."""
+    n = 1 << log_n
+    basis = nt.RnsBasis.build(n, bits, 2, seed=4)
+    B = 2
+    A = np.stack([np.stack([rand(q, n, 5 * b + l) for l, q in enumerate(basis.primes)])
+                  for b in range(B)])
+    Bm = np.stack([np.stack([rand(q, n, 50 + 5 * b + l) for l, q in enumerate(basis.primes)])
+                   for b in range(B)])
+    # adversarial extremes: all q-1
+    A[0, 0, :] = basis.primes[0] - 1
+    Bm[0, 0, :] = basis.primes[0] - 1
+    got = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
+    want = oracle.polymul_rns(A, Bm, basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(got, want)
+    plan = basis.plans[1]
+    f, v = oracle.twiddles(plan.q, plan.psi, log_n)
+    x = A[1, 1].copy()
+    t = dev(x)
+    K.ntt_ct(t, plan.tw_fwd, *plan.red_args, False)
+    w = x.copy()
+    oracle.ntt_ct(w, f, *plan.red_args, False)
+    assert np.array_equal(host(t), w)
+    K.intt_gs(t, plan.tw_inv, plan.q, (plan.q + 1) // 2, *plan.red_args[1:], True, False)
+    assert np.array_equal(host(t), x)
