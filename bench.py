@@ -293,7 +293,7 @@ def main():
     # ---- e2e: public API with pinned host buffers, copies inside timing ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(nt, basis, A_h, B_h, args, world, stream)
+        e2e = run_e2e(nt, basis, A_h, B_h, args, world, stream, C)
 
     # ---- parity spot check + CPU baseline (rank 0, N=1 only) ----
     cpu = None
@@ -330,20 +330,17 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(nt, basis, A_h, B_h, args, world, stream):
+def run_e2e(nt, basis, A_h, B_h, args, world, stream, C_dev):
     import torch
 
     Ap = torch.from_numpy(A_h).pin_memory()
     Bp = torch.from_numpy(B_h).pin_memory()
     Cp = torch.empty_like(Ap).pin_memory()
-    Ad, Bd = torch.empty_like(Ap, device="cuda"), torch.empty_like(Bp, device="cuda")
-    Cd, Wd = torch.empty_like(Ad), torch.empty_like(Ad)
 
     def one():
-        Ad.copy_(Ap, non_blocking=True)
-        Bd.copy_(Bp, non_blocking=True)
-        nt.polymul_rns_batch(Ad, Bd, basis, out=Cd, workspace=Wd)
-        Cp.copy_(Cd, non_blocking=True)
+        # the public API with host buffers: chunked H2D / kernels / D2H overlap
+        # inside nttmul_polymul_fused_rns_host; returns when Cp holds c
+        nt.polymul_rns_batch(Ap, Bp, basis, out=Cp)
 
     steps = max(3, min(args.steps, 10))
     for _ in range(2):
@@ -362,10 +359,12 @@ def run_e2e(nt, basis, A_h, B_h, args, world, stream):
 
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    same = torch.equal(Cp, C_dev.cpu())  # streamed host result == device-resident result
     return {"value": round(world * A_h.shape[0] * steps / (ms / 1e3), 2), "unit": UNIT,
             "h2d_bytes_per_step": int(A_h.nbytes + B_h.nbytes),
             "d2h_bytes_per_step": int(A_h.nbytes), "steps": steps,
-            "path": "polymul_rns_batch(pinned host -> HBM -> C ABI -> pinned host)"}
+            "parity_vs_device": "bit-exact" if same else "MISMATCH",
+            "path": "polymul_rns_batch(pinned host tensors) -> nttmul_polymul_fused_rns_host (chunked H2D / fused kernels / D2H on 3 streams) -> pinned host"}
 
 
 def modmul_roof(nt, basis, stream):

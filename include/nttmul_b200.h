@@ -217,6 +217,29 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a,
                                     void *stream);
 
 /*
+ * Same product over HOST buffers (c_host, a_host, b_host: [batch, num_limbs,
+ * 2^log_n] uint64, pinned for full overlap).  This is the call the reference's
+ * own entry point corresponds to (polymul_rns over numpy arrays,
+ * rns.py:111-120, with polymul_batch's ciphertext loop polymul.py:175-207):
+ * host arrays in, host array out.  The batch is streamed in chunks of
+ * `chunk_cts` ciphertexts through NTTMUL_HOST_NBUF device buffer sets in
+ * `dev_buf` (>= NTTMUL_HOST_NBUF * 4 * chunk_cts * num_limbs * 2^log_n words,
+ * 16-byte aligned); host->device copies, the fused kernels and device->host
+ * copies of different chunks overlap on three streams.  Work is ordered after
+ * everything already queued on `stream`, and `stream` completes when c_host
+ * holds the full result.
+ */
+#define NTTMUL_HOST_NBUF 3
+int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
+                                  const uint64_t *b_host,
+                                  const nttmul_limb_t *limbs,
+                                  const uint64_t *fwd_pairs,
+                                  const uint64_t *inv_pairs, int log_n,
+                                  int num_limbs, int64_t batch, int mode,
+                                  uint64_t *dev_buf, int64_t chunk_cts,
+                                  void *stream);
+
+/*
  * Pipeline knob of nttmul_polymul_fused_rns for n > 4096 (process-wide):
  * the batch is processed in chunks of `chunk_waves` fused-row-kernel waves
  * whose intermediates stay in L2 (scratch lines are discarded once read, so

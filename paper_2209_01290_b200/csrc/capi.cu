@@ -637,6 +637,80 @@ int nttmul_polymul_fused_rns(uint64_t *c, const uint64_t *a, const uint64_t *b,
                                          num_limbs, batch, mode, workspace, 7, stream);
 }
 
+// Host-buffer product: chunks of `chunk_cts` ciphertexts flow through NBUF
+// device buffer sets; H2D (own stream), the fused kernels (caller's stream)
+// and D2H (own stream) of different chunks overlap, so the call is bound by
+// the slower PCIe direction instead of the sum of copies and compute.
+int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
+                                  const uint64_t *b_host, const nttmul_limb_t *limbs,
+                                  const uint64_t *fwd_pairs, const uint64_t *inv_pairs,
+                                  int log_n, int num_limbs, int64_t batch, int mode,
+                                  uint64_t *dev_buf, int64_t chunk_cts, void *stream) {
+  constexpr int NBUF = NTTMUL_HOST_NBUF;
+  CHECK(check_log_n(log_n, 2));
+  if (num_limbs < 1) return fail(NTTMUL_EINVAL, "num_limbs < 1");
+  if (batch < 0 || chunk_cts < 1) return fail(NTTMUL_EINVAL, "batch < 0 or chunk_cts < 1");
+  if (batch == 0) return NTTMUL_OK;
+  if (!c_host || !a_host || !b_host) return fail(NTTMUL_EPTR, "host buffer is NULL");
+  CHECK(check_dev(dev_buf, 16, "dev_buf"));
+  struct Pipe {
+    cudaStream_t s_in, s_out;
+    cudaEvent_t ev_start, ev_in[NBUF], ev_done[NBUF], ev_out[NBUF];
+  };
+  static Pipe pipes[64];  // one set of copy streams / events per device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cuda_status("device");
+  Pipe &pp = pipes[dev];
+  cudaStream_t &s_in = pp.s_in, &s_out = pp.s_out;
+  cudaEvent_t &ev_start = pp.ev_start, *ev_in = pp.ev_in, *ev_done = pp.ev_done,
+              *ev_out = pp.ev_out;
+  if (!s_in) {
+    if (cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_status("host pipeline streams");
+    for (int i = 0; i < NBUF; ++i)
+      if (cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming) != cudaSuccess)
+        return cuda_status("host pipeline events");
+  }
+  const cudaStream_t sc = S(stream);
+  const long long per_ct = static_cast<long long>(num_limbs) << log_n;  // words
+  const long long set_words = 4 * chunk_cts * per_ct;                    // a, b, c, ws
+  // copies of chunk i start only after everything queued on the caller's
+  // stream before this call (the caller's timing events bracket the call)
+  if (cudaEventRecord(ev_start, sc) != cudaSuccess || cudaStreamWaitEvent(s_in, ev_start) != cudaSuccess)
+    return cuda_status("host pipeline start");
+  const long long nchunks = (batch + chunk_cts - 1) / chunk_cts;
+  for (long long i = 0; i < nchunks; ++i) {
+    const int s = static_cast<int>(i % NBUF);
+    const long long cts = (i + 1) * chunk_cts > batch ? batch - i * chunk_cts : chunk_cts;
+    const size_t bytes = static_cast<size_t>(cts * per_ct) * sizeof(u64);
+    const long long off = i * chunk_cts * per_ct;
+    u64 *da = dev_buf + s * set_words, *db = da + chunk_cts * per_ct;
+    u64 *dc = db + chunk_cts * per_ct, *dw = dc + chunk_cts * per_ct;
+    if (i >= NBUF && cudaStreamWaitEvent(s_in, ev_done[s]) != cudaSuccess)  // a, b consumed
+      return cuda_status("host pipeline wait");
+    if (cudaMemcpyAsync(da, a_host + off, bytes, cudaMemcpyHostToDevice, s_in) != cudaSuccess ||
+        cudaMemcpyAsync(db, b_host + off, bytes, cudaMemcpyHostToDevice, s_in) != cudaSuccess ||
+        cudaEventRecord(ev_in[s], s_in) != cudaSuccess || cudaStreamWaitEvent(sc, ev_in[s]) != cudaSuccess)
+      return cuda_status("host pipeline H2D");
+    if (i >= NBUF && cudaStreamWaitEvent(sc, ev_out[s]) != cudaSuccess)  // c drained
+      return cuda_status("host pipeline wait");
+    CHECK(nttmul_polymul_fused_rns(dc, da, db, limbs, fwd_pairs, inv_pairs, log_n, num_limbs,
+                                   cts, mode, dw, stream));
+    if (cudaEventRecord(ev_done[s], sc) != cudaSuccess || cudaStreamWaitEvent(s_out, ev_done[s]) != cudaSuccess ||
+        cudaMemcpyAsync(c_host + off, dc, bytes, cudaMemcpyDeviceToHost, s_out) != cudaSuccess ||
+        cudaEventRecord(ev_out[s], s_out) != cudaSuccess)
+      return cuda_status("host pipeline D2H");
+  }
+  // the caller's stream completes when the last result has landed in c_host
+  const int last = static_cast<int>((nchunks - 1) % NBUF);
+  if (cudaStreamWaitEvent(sc, ev_out[last]) != cudaSuccess) return cuda_status("host pipeline end");
+  return NTTMUL_OK;
+}
+
 int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int threads,
                        int64_t iters, uint64_t *sink_out, double *modmuls_out,
                        void *stream) {

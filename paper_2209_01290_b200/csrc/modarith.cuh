@@ -22,12 +22,28 @@ namespace nttb {
 typedef uint64_t u64;
 typedef nttmul_limb_t Limb;
 
-// x >= m ? x - m : x, for x < m + 2^63 (sign test on the wrapped difference:
-// IADD3 + IADD3.X + 2 SEL, no 64-bit compare).
+// x >= m ? x - m : x.
+// NTTB_CSUB_CARRY: the borrow of the 64-bit subtraction (a PTX carry chain)
+// selects the result - IADD3 + IADD3.X (carry out) + 2 predicated moves, but
+// the extra live borrow register raises spills in the row kernel.
+#ifdef NTTB_CSUB_CARRY
+__device__ __forceinline__ u64 csub(u64 x, u64 m) {
+  uint32_t tl, th, br;
+  asm("sub.cc.u32 %0, %3, %5;\n\t"
+      "subc.cc.u32 %1, %4, %6;\n\t"
+      "subc.u32 %2, 0, 0;"
+      : "=r"(tl), "=r"(th), "=r"(br)
+      : "r"(static_cast<uint32_t>(x)), "r"(static_cast<uint32_t>(x >> 32)),
+        "r"(static_cast<uint32_t>(m)), "r"(static_cast<uint32_t>(m >> 32)));
+  return br ? x : ((static_cast<u64>(th) << 32) | tl);
+}
+#else
+// sign-test form (valid for x < m + 2^63): IADD3 + IADD3.X + ISETP + 2 SEL
 __device__ __forceinline__ u64 csub(u64 x, u64 m) {
   const u64 t = x - m;
   return (static_cast<long long>(t) < 0) ? x : t;
 }
+#endif
 
 // Barrett data x data product, a, b canonical.  MODE: NTTMUL_RED_*.
 template <int MODE>
@@ -86,13 +102,37 @@ __device__ __forceinline__ Mod make_mod(u64 q) {
   return m;
 }
 
+// floor(x * y / 2^64) - e, e in {0, 1}: the high word from three of the
+// four 32x32 partial products (x_lo * y_lo, < 2^64, is dropped).  The
+// middle column x_hi y_lo + x_lo y_hi is summed exactly as
+// (x_hi y_lo + lo32(x_lo y_hi)) + hi32(x_lo y_hi) 2^32.
+// 3 IMAD.WIDE.U32 + one 64-bit add.
+__device__ __forceinline__ u64 mulhi_approx(u64 x, u64 y) {
+  const uint32_t xl = lo32(x), xh = hi32(x);
+  const u64 b = mulw(xl, hi32(y));
+  const u64 c = madw(xh, lo32(y), lo32(b));  // <= (2^32-1)^2 + 2^32-1 < 2^64
+  return madw(xh, hi32(y), hi32(b)) + hi32(c);
+}
+
+// x * y mod 2^64 + a as 32-bit pieces: 1 IMAD.WIDE.U32 + 2 IMAD
+__device__ __forceinline__ u64 mullo_add(uint32_t xl, uint32_t xh, uint32_t yl, uint32_t yh,
+                                         u64 a) {
+  const u64 t = madw(xl, yl, a);
+  uint32_t h = hi32(t);
+  h = xl * yh + h;
+  h = xh * yl + h;
+  return (static_cast<u64>(h) << 32) | lo32(t);
+}
+
 // Shoup product x * w mod q in [0, 4q) for any x < 2^64 (w < q,
 // wp = floor(w 2^64 / q)).  The quotient uses three of the four partial
 // products of x * wp (the x_lo * wp_lo term and the low halves of the cross
 // terms are dropped): it undershoots floor(x wp / 2^64) by at most 2, so the
 // remainder lands in [0, 4q) instead of [0, 2q).  The remainder is formed as
 // x*w + qh*(2^64 - q) mod 2^64 so every step is a multiply-accumulate:
-// 5 IMAD.WIDE.U32 + 4 IMAD + one 64-bit add.
+// 5 IMAD.WIDE.U32 + 4 IMAD + one 64-bit add.  (Measured faster than the
+// mulhi_approx chain below inside the butterflies: ptxas schedules the two
+// independent cross products better.)
 __device__ __forceinline__ u64 shoup4(u64 x, u64 w, u64 wp, const Mod &M) {
   const uint32_t xl = lo32(x), xh = hi32(x);
   const u64 b = mulw(xl, hi32(wp));
@@ -106,6 +146,25 @@ __device__ __forceinline__ u64 shoup4(u64 x, u64 w, u64 wp, const Mod &M) {
   h = ql * M.nqh + h;
   h = qhh * M.nql + h;
   return (static_cast<u64>(h) << 32) | lo32(a);
+}
+
+// Lazy Barrett data x data product for the paper's proposed-shape constants
+// (mode NTTMUL_RED_ONE_SUB: proposed or dhem, modulus m <= 60 bits): a * b < 4 q^2
+// (e.g. a, b < 2q).  T = a b exactly (4 IMAD.WIDE.U32 in a carry-free
+// chain); c = T >> s_in (< 2^64); quot = hi64(c mu_sh) - e (mulhi_approx)
+// undershoots floor(T / q) by at most 4 (Barrett's own <= 1 for canonical
+// inputs, < 2 more from c < 2^(m+4), 1 from the approximate high word), so
+// r = T - quot q lies in [0, 5q).  8 IMAD.WIDE.U32 + 2 IMAD in total.
+__device__ __forceinline__ u64 mulred_lazy(u64 a, u64 b, const Limb &L, const Mod &M) {
+  const uint32_t al = lo32(a), ah = hi32(a), bl = lo32(b), bh = hi32(b);
+  const u64 p0 = mulw(al, bl);
+  const u64 p1 = madw(al, bh, hi32(p0));
+  const u64 p2 = madw(ah, bl, lo32(p1));
+  const u64 tlo = (static_cast<u64>(lo32(p2)) << 32) | lo32(p0);
+  const u64 thi = madw(ah, bh, hi32(p1)) + hi32(p2);
+  const u64 c = (tlo >> L.s_in) | ((thi << 1) << (63 - L.s_in));
+  const u64 quot = mulhi_approx(c, L.mu_sh) >> L.s_hi;
+  return mullo_add(lo32(quot), hi32(quot), M.nql, M.nqh, tlo);
 }
 
 // ---- butterflies ----------------------------------------------------------
@@ -218,6 +277,31 @@ __device__ __forceinline__ void fused_pair(u64 a0, u64 a1, u64 b0, u64 b1,
   c1 = csub(y + q - v, q);
   const u64 z = shoup(v, w, wp, M);
   c0 = odd ? csub(u + q - z, q) : csub(u + z, q);
+}
+
+// forward-range value (LB = 16) -> [0, 2q)
+__device__ __forceinline__ u64 to2q_fwd16(u64 x, const Mod &M) {
+  return csub(csub(csub(x, M.q8), M.q4), M.q2);
+}
+
+// Lazy Karatsuba-fused middle pair for the LB = 16 path (all q < 2^60,
+// proposed-shape Barrett constants): inputs in [0, 2q), outputs c0, c1 in
+// [0, 4q) (the inverse lazy range, so the inverse stages take them as is).
+// Same algebra as fused_pair / reference _kernels.pyx:142-173; canonical
+// results after the inverse transform are identical.
+__device__ __forceinline__ void fused_pair_lazy(u64 a0, u64 a1, u64 b0, u64 b1, u64 w, u64 wp,
+                                                bool odd, const Limb &L, const Mod &M,
+                                                u64 &c0, u64 &c1) {
+  const u64 u = mulred_lazy(a0, b0, L, M);         // [0, 5q)
+  const u64 v = mulred_lazy(a1, b1, L, M);         // [0, 5q)
+  const u64 s1 = csub(a0 + a1, M.q2);              // [0, 2q)
+  const u64 s2 = csub(b0 + b1, M.q2);
+  const u64 ww = mulred_lazy(s1, s2, L, M);        // [0, 5q)
+  const u64 y = ww + M.q8 + M.q2 - u - v;          // (0, 15q)
+  c1 = csub(csub(y, M.q8), M.q4);                  // [0, 4q)
+  const u64 z = shoup4(v, w, wp, M);               // [0, 4q)
+  const u64 x = odd ? u + M.q4 - z : u + z;        // [0, 9q)
+  c0 = csub(csub(x, M.q8), M.q4);                  // [0, 4q)
 }
 
 }  // namespace nttb

@@ -106,6 +106,9 @@ enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 #ifndef NTTB_PREFETCH_B
 #define NTTB_PREFETCH_B 1
 #endif
+#ifndef NTTB_LAZY_MID
+#define NTTB_LAZY_MID 1
+#endif
 
 template <int LOG_R, int LOG_E = NTTB_ROW_LOG_E>
 struct RowGeom {
@@ -301,6 +304,8 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   using G = RowGeom<LOG_R>;
   constexpr int E = G::E;
   constexpr int LE = G::HEAD == 0 ? 0 : LOG_R - G::HEAD;  // = LOG_E
+  // lazy Barrett middle (proposed/dhem constants, all moduli < 2^60)
+  constexpr bool LAZY_MID = NTTB_LAZY_MID && MODE == NTTMUL_RED_ONE_SUB && LB == 16;
   const int o0 = threadIdx.x * E;
   const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
 #ifdef NTTB_TW_PREFETCH
@@ -319,7 +324,8 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
     fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
 #endif
 #pragma unroll
-    for (int e = 0; e < E; ++e) sm[G::idx(o0 + e)] = canon_fwd<LB>(xa[0][e], M);
+    for (int e = 0; e < E; ++e)
+      sm[G::idx(o0 + e)] = LAZY_MID ? to2q_fwd16(xa[0][e], M) : canon_fwd<LB>(xa[0][e], M);
 #pragma unroll
     for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + G::idx(o0 + e)];
 #ifdef NTTB_TW_PREFETCH
@@ -337,9 +343,14 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i0 = 2 * (p + h);
-        fused_pair<MODE>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
-                         canon_fwd<LB>(xa[0][i0], M), canon_fwd<LB>(xa[0][i0 + 1], M),
-                         w.x, w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
+        if constexpr (LAZY_MID)
+          fused_pair_lazy(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
+                          to2q_fwd16(xa[0][i0], M), to2q_fwd16(xa[0][i0 + 1], M), w.x, w.y,
+                          h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
+        else
+          fused_pair<MODE>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
+                           canon_fwd<LB>(xa[0][i0], M), canon_fwd<LB>(xa[0][i0 + 1], M),
+                           w.x, w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
       }
     }
 #ifdef NTTB_TW_PREFETCH

@@ -239,6 +239,34 @@ def test_rns_cfg3_one_ciphertext(golden):
     assert np.array_equal(got, want)
 
 
+def test_rns_host_buffers_streamed(golden):
+    """Host (pinned and unpinned) [B, L, n] inputs stream through the
+    chunked H2D / kernel / D2H pipeline: more chunks than device buffer sets,
+    a ragged last chunk, results identical to the device-resident call."""
+    g = next(b for b in golden["bases"] if b["n"] == 1 << 14)
+    basis = nt.RnsBasis.build(g["n"], g["bits"], g["k"], seed=0)
+    B, L, n = 7, g["k"], g["n"]
+    A = np.stack([np.stack([rand(q, n, 31 * b + l) for l, q in enumerate(basis.primes)])
+                  for b in range(B)])
+    Bm = np.stack([np.stack([rand(q, n, 577 + 31 * b + l) for l, q in enumerate(basis.primes)])
+                   for b in range(B)])
+    want = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
+    assert np.array_equal(want[:2], oracle.polymul_rns(A[:2], Bm[:2], basis.primes,
+                                                       [p.psi for p in basis.plans]))
+    old = nt.rns.HOST_CHUNK_BYTES
+    try:
+        nt.rns.HOST_CHUNK_BYTES = 2 * L * n * 8  # 2 ciphertexts per chunk -> 4 chunks
+        got = nt.polymul_rns_batch(torch.from_numpy(A).pin_memory(),
+                                   torch.from_numpy(Bm).pin_memory(), basis)
+        assert not got.is_cuda and np.array_equal(got.numpy(), want)
+        got2 = nt.polymul_rns_batch(A, Bm, basis)  # numpy, unpinned
+        assert np.array_equal(got2.numpy(), want)
+    finally:
+        nt.rns.HOST_CHUNK_BYTES = old
+    empty = nt.polymul_rns_batch(A[:0], Bm[:0], basis)
+    assert tuple(empty.shape) == (0, L, n)
+
+
 def test_rns_bigint_end_to_end():
     basis = nt.RnsBasis.build(64, 30, 4, seed=2)
     import random
