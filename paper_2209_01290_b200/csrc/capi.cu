@@ -85,13 +85,31 @@ int smem_optin(K kernel, size_t bytes) {
 }
 
 // ---- row kernel dispatch ---------------------------------------------------
+#ifndef NTTB_ROW_PF
+#define NTTB_ROW_PF 1  // L2 prefetch of the rows one resident wave ahead
+#endif
 template <int LOG_R, int FWD, bool MID, int INV, int MODE, int LB>
 int launch_row_t(const RowParams &P, long long rows, cudaStream_t st) {
   constexpr int NP = MID ? 2 : 1;
   const size_t smem = NP * RowGeom<LOG_R>::PADN * sizeof(u64);
   auto k = row_kernel<LOG_R, FWD, MID, INV, MODE, LB>;
   CHECK(smem_optin(k, smem));
-  k<<<static_cast<unsigned>(rows), RowGeom<LOG_R>::T, smem, st>>>(P);
+  static long long slots = 0;  // resident CTAs per device for this instantiation
+  if (!slots) {
+    int dev = 0, sms = 148, nb = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, RowGeom<LOG_R>::T, smem) !=
+            cudaSuccess || nb < 1) {
+      cudaGetLastError();
+      nb = 1;
+    }
+    slots = static_cast<long long>(nb) * sms;
+  }
+  RowParams Q = P;
+  Q.nrows = rows;
+  Q.pf_dist = NTTB_ROW_PF ? slots : 0;
+  k<<<static_cast<unsigned>(rows), RowGeom<LOG_R>::T, smem, st>>>(Q);
   return cuda_status("row_kernel");
 }
 
@@ -146,8 +164,44 @@ int launch_row_fused(int log_r, const RowParams &P, long long rows, cudaStream_t
 }
 
 // ---- column kernel dispatch -------------------------------------------------
+#ifndef NTTB_COL_PIPE
+#define NTTB_COL_PIPE 0  // 1: bulk-copy pipelined column kernel (measured no faster, sweep_r16)
+#endif
+template <int LOG_N1, bool INV, int LB>
+int launch_col_pipe_t(const ColParams &P, cudaStream_t st) {
+  using G = ColPipeGeom<LOG_N1>;
+  auto k = col_pipe_kernel<LOG_N1, INV, LB>;
+  CHECK(smem_optin(k, G::SMEM));
+  static int slots = 0;  // resident CTAs per device for this instantiation
+  if (!slots) {
+    int dev = 0, sms = 148, nb = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, G::TC, G::SMEM) != cudaSuccess ||
+        nb < 1) {
+      cudaGetLastError();
+      nb = 1;
+    }
+    slots = nb * sms;
+  }
+  const long long tiles = P.nsrc * P.npolys * G::TILES_PER_POLY;
+  const long long grid = tiles < slots ? tiles : slots;
+  if (grid == 0) return NTTMUL_OK;
+  k<<<static_cast<unsigned>(grid), G::TC, G::SMEM, st>>>(P);
+  return cuda_status("col_pipe_kernel");
+}
+
 template <bool INV, int LB>
 int launch_col(int log_n1, const ColParams &P, cudaStream_t st) {
+  if (NTTB_COL_PIPE && !P.discard_src && COL_LOG_R == 12) {
+    switch (log_n1) {
+      case 1: return launch_col_pipe_t<1, INV, LB>(P, st);
+      case 2: return launch_col_pipe_t<2, INV, LB>(P, st);
+      case 3: return launch_col_pipe_t<3, INV, LB>(P, st);
+      case 4: return launch_col_pipe_t<4, INV, LB>(P, st);
+      case 5: return launch_col_pipe_t<5, INV, LB>(P, st);
+    }
+  }
   const unsigned grid = static_cast<unsigned>(
       (P.nsrc * ((P.npolys << COL_LOG_R) / COL_VEC) + COL_THREADS - 1) / COL_THREADS);
   switch (log_n1) {

@@ -84,6 +84,23 @@ __device__ __forceinline__ u64 madw(uint32_t a, uint32_t b, u64 c) {
   return d;
 }
 
+// 32-bit multiply-add and {lo, hi} packing in PTX.  Written as C++
+// (`(u64)h << 32 | lo` with h = sum of products) the composition is
+// re-associated by the compiler into a 64-bit add whose low half adds zero
+// (a wasted IADD3 + IMAD.X per product); the explicit forms keep it to the
+// 32-bit IMAD chain.
+__device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ u64 pack(uint32_t lo, uint32_t hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
 // Per-prime constants the butterflies need.
 struct Mod {
   u64 q, q2, q4, q8;
@@ -119,9 +136,9 @@ __device__ __forceinline__ u64 mullo_add(uint32_t xl, uint32_t xh, uint32_t yl, 
                                          u64 a) {
   const u64 t = madw(xl, yl, a);
   uint32_t h = hi32(t);
-  h = xl * yh + h;
-  h = xh * yl + h;
-  return (static_cast<u64>(h) << 32) | lo32(t);
+  h = madlo(xl, yh, h);
+  h = madlo(xh, yl, h);
+  return pack(lo32(t), h);
 }
 
 // Shoup product x * w mod q in [0, 4q) for any x < 2^64 (w < q,
@@ -141,11 +158,11 @@ __device__ __forceinline__ u64 shoup4(u64 x, u64 w, u64 wp, const Mod &M) {
   const uint32_t ql = lo32(qh), qhh = hi32(qh);
   const u64 a = madw(ql, M.nql, mulw(xl, lo32(w)));
   uint32_t h = hi32(a);
-  h = xl * hi32(w) + h;
-  h = xh * lo32(w) + h;
-  h = ql * M.nqh + h;
-  h = qhh * M.nql + h;
-  return (static_cast<u64>(h) << 32) | lo32(a);
+  h = madlo(xl, hi32(w), h);
+  h = madlo(xh, lo32(w), h);
+  h = madlo(ql, M.nqh, h);
+  h = madlo(qhh, M.nql, h);
+  return pack(lo32(a), h);
 }
 
 // Lazy Barrett data x data product for the paper's proposed-shape constants
@@ -160,7 +177,7 @@ __device__ __forceinline__ u64 mulred_lazy(u64 a, u64 b, const Limb &L, const Mo
   const u64 p0 = mulw(al, bl);
   const u64 p1 = madw(al, bh, hi32(p0));
   const u64 p2 = madw(ah, bl, lo32(p1));
-  const u64 tlo = (static_cast<u64>(lo32(p2)) << 32) | lo32(p0);
+  const u64 tlo = pack(lo32(p0), lo32(p2));
   const u64 thi = madw(ah, bh, hi32(p1)) + hi32(p2);
   const u64 c = (tlo >> L.s_in) | ((thi << 1) << (63 - L.s_in));
   const u64 quot = mulhi_approx(c, L.mu_sh) >> L.s_hi;

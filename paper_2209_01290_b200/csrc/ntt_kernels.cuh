@@ -109,6 +109,11 @@ enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 #ifndef NTTB_LAZY_MID
 #define NTTB_LAZY_MID 1
 #endif
+// issue a unit's twiddle loads before its data loads (hides their L2
+// latency; measured -2.7 % row-kernel time, sweep_r18)
+#ifndef NTTB_TW_PREFETCH
+#define NTTB_TW_PREFETCH 1
+#endif
 
 template <int LOG_R, int LOG_E = NTTB_ROW_LOG_E>
 struct RowGeom {
@@ -144,7 +149,14 @@ struct RowParams {
   int log_n1;  // rows per polynomial = 2^log_n1
   int fin;     // FinalMode of the global last inverse stage (if in this kernel)
   int discard_in;  // inputs are pipeline scratch: discard their L2 lines once read
+  long long nrows;    // rows in this launch
+  long long pf_dist;  // > 0: prefetch the input rows of row + pf_dist into L2
 };
+
+// bulk prefetch of [p, p + bytes) into L2 (no register or smem cost)
+__device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 // forward head pass: R stages starting at row-local stage S0.  The NP
 // polynomials are processed one after the other (the second pass over the
@@ -168,7 +180,7 @@ __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
       const int u = threadIdx.x + w * G::T;
       const int grp = u >> LK;
       const int o0 = (grp << (LOG_R - S0)) + (u & ((1 << LK) - 1));
-#ifdef NTTB_TW_PREFETCH
+#if NTTB_TW_PREFETCH
       TwBuf<0, R> twb;
       tw_prefetch(twb, tw, (rowbase << S0) + grp);
 #endif
@@ -178,7 +190,7 @@ __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
         const int o = o0 + (e << LK);
         x[0][e] = FROM_GLOBAL ? g[o] : s[G::idx(o)];
       }
-#ifdef NTTB_TW_PREFETCH
+#if NTTB_TW_PREFETCH
       fwd_radix_pf<LB, R, R, 1, S0 & 1>(x, twb, M);
 #else
       fwd_radix<LB, R, R, 1, S0 & 1>(x, (rowbase << S0) + grp, tw, M);
@@ -204,7 +216,7 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
     const int g = u >> LK;
     const int o0 = (g << (LOG_R - S0)) + (u & ((1 << LK) - 1));
     const u64 B0 = (rowbase << S0) + g;
-#ifdef NTTB_TW_PREFETCH
+#if NTTB_TW_PREFETCH
     TwBuf<0, R> twb;
     tw_prefetch(twb, tw, B0);
 #endif
@@ -212,7 +224,7 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
 #pragma unroll
     for (int e = 0; e < (1 << R); ++e) x[0][e] = sm[G::idx(o0 + (e << LK))];
     if (TO_GLOBAL) {
-#ifdef NTTB_TW_PREFETCH
+#if NTTB_TW_PREFETCH
       inv_radix_pf<LB, R, R, 1, 1>(x, twb, M);
 #else
       inv_radix<LB, R, R, 1, 1>(x, B0, tw, M);
@@ -221,7 +233,7 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
 #pragma unroll
       for (int e = 0; e < (1 << R); ++e) gout[o0 + (e << LK)] = x[0][e];
     } else {
-#ifdef NTTB_TW_PREFETCH
+#if NTTB_TW_PREFETCH
       inv_radix_pf<LB, R, R, 0, 1>(x, twb, M);
 #else
       inv_radix<LB, R, R, 0, 1>(x, B0, tw, M);
@@ -308,7 +320,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   constexpr bool LAZY_MID = NTTB_LAZY_MID && MODE == NTTMUL_RED_ONE_SUB && LB == 16;
   const int o0 = threadIdx.x * E;
   const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
-#ifdef NTTB_TW_PREFETCH
+#if NTTB_TW_PREFETCH
   TwBuf<0, LE - 1> twb;
   if constexpr (MID) tw_prefetch(twb, twf, B0);
 #endif
@@ -318,7 +330,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   if constexpr (MID) {
     // a's last truncated stages first, parked (canonical) in its own smem
     // slots; then b's, kept in registers and overwritten by c pair by pair.
-#ifdef NTTB_TW_PREFETCH
+#if NTTB_TW_PREFETCH
     fwd_radix_pf<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, twb, M);
 #else
     fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
@@ -328,7 +340,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
       sm[G::idx(o0 + e)] = LAZY_MID ? to2q_fwd16(xa[0][e], M) : canon_fwd<LB>(xa[0][e], M);
 #pragma unroll
     for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + G::idx(o0 + e)];
-#ifdef NTTB_TW_PREFETCH
+#if NTTB_TW_PREFETCH
     fwd_radix_pf<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, twb, M);
     tw_prefetch(twb, twi, B0);  // inverse twiddles of the same groups
 #else
@@ -353,7 +365,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
                            w.x, w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
       }
     }
-#ifdef NTTB_TW_PREFETCH
+#if NTTB_TW_PREFETCH
     inv_radix_pf<LB, LE, LE - 1, 0, 1>(xa, twb, M);
 #else
     inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
@@ -431,6 +443,14 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
   const u64 rowbase = (1ULL << P.log_n1) + r;  // (N1 + r): group index base
   const long long off = row * G::N2;
   NTTB_STAMP(0);
+  // Rows are dispatched in order, so the CTA that takes row + pf_dist (one
+  // resident wave later) starts about when this one ends: pull its inputs
+  // into L2 now so its first pass does not wait on HBM latency.
+  if (FWD != FWD_NONE && P.pf_dist > 0 && threadIdx.x == 0 && row + P.pf_dist < P.nrows) {
+    const long long nx = (row + P.pf_dist) * G::N2;
+    prefetch_l2(P.in0 + nx, G::N2 * sizeof(u64));
+    if (NP > 1) prefetch_l2(P.in1 + nx, G::N2 * sizeof(u64));
+  }
 
   if (MID && NTTB_PREFETCH_B) {
     // b's row streams into its smem slot (cp.async) while a's first pass
@@ -623,6 +643,165 @@ __global__ void __launch_bounds__(COL_THREADS, NTTB_COL_MINB) col_kernel(const C
       dst[o] = x[0][e];
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// PIPELINED COLUMN kernel (default for n > 4096).
+//
+// The plain column kernel above is latency-bound: each thread's 2 x N1
+// strided loads must land before any arithmetic, and 128 registers per
+// thread cap residency at 16 warps per SM.  Here a persistent CTA streams
+// column TILES (N1 rows x TC columns, rows contiguous TC*8-byte segments)
+// through a STAGES-deep shared-memory ring with the bulk-copy engine
+// (cp.async.bulk global->shared, completion counted on an mbarrier), so
+// the next tiles are in flight while the current one is transformed; results
+// go back through the same buffer with bulk shared->global stores.  One
+// thread owns one column (N1 values in registers); a warp reads 32
+// consecutive words of a row - conflict-free.
+
+namespace bulk {
+__device__ __forceinline__ unsigned saddr(const void *p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(u64 *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64 *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(saddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void load(void *dst, const void *src, unsigned bytes, u64 *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void store(void *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(saddr(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+}  // namespace bulk
+
+#ifndef NTTB_COLPIPE_TC
+#define NTTB_COLPIPE_TC 256
+#endif
+#ifndef NTTB_COLPIPE_STAGES
+#define NTTB_COLPIPE_STAGES 2
+#endif
+template <int LOG_N1>
+struct ColPipeGeom {
+  static constexpr int N1 = 1 << LOG_N1;
+  static constexpr int TC = LOG_N1 >= 5 ? 128 : NTTB_COLPIPE_TC;  // columns per tile = threads
+  static constexpr int STAGES = NTTB_COLPIPE_STAGES;
+  static constexpr int TILE_WORDS = N1 * TC;
+  static constexpr int TILES_PER_POLY = (1 << COL_LOG_R) / TC;
+  static constexpr size_t SMEM = STAGES * TILE_WORDS * sizeof(u64) + 64;  // + barriers
+};
+
+template <int LOG_N1, bool INV, int LB>
+__global__ void __launch_bounds__(ColPipeGeom<LOG_N1>::TC)
+    col_pipe_kernel(const ColParams P) {
+  using G = ColPipeGeom<LOG_N1>;
+  constexpr int N1 = G::N1, TC = G::TC, S = G::STAGES;
+  constexpr unsigned ROW_BYTES = TC * sizeof(u64);
+  extern __shared__ __align__(128) u64 csm[];
+  u64 *bars = csm + S * G::TILE_WORDS;
+  const long long per_src = P.npolys * G::TILES_PER_POLY;
+  const long long ntiles = per_src * P.nsrc;
+  // tile -> (source, polynomial, first column)
+  auto where = [&](long long t, int &which, long long &poly, int &col0) {
+    which = t >= per_src ? 1 : 0;
+    const long long r = t - (which ? per_src : 0);
+    poly = r / G::TILES_PER_POLY;
+    col0 = static_cast<int>(r % G::TILES_PER_POLY) * TC;
+  };
+  auto issue_load = [&](long long t, int s) {
+    int which, col0;
+    long long poly;
+    where(t, which, poly, col0);
+    const u64 *src = (which ? P.src1 : P.src0) + (poly << (COL_LOG_R + LOG_N1)) + col0;
+    bulk::mbar_expect_tx(bars + s, N1 * ROW_BYTES);
+#pragma unroll 1
+    for (int e = 0; e < N1; ++e)
+      bulk::load(csm + s * G::TILE_WORDS + e * TC, src + (static_cast<long long>(e) << COL_LOG_R),
+                 ROW_BYTES, bars + s);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) bulk::mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < S; ++s) {
+      const long long t = blockIdx.x + static_cast<long long>(s) * gridDim.x;
+      if (t < ntiles) issue_load(t, s);
+    }
+  int it = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % S;
+    int which, col0;
+    long long poly;
+    where(t, which, poly, col0);
+    int limb;
+    const Limb &L = *limb_ptr(P.limbs, poly, limb);
+    const Mod M = make_mod(L.q);
+    u64 *buf = csm + s * G::TILE_WORDS;
+    bulk::mbar_wait(bars + s, (it / S) & 1);
+    u64 x[1][N1];
+#pragma unroll
+    for (int e = 0; e < N1; ++e) x[0][e] = buf[e * TC + threadIdx.x];
+    if (!INV) {
+      fwd_radix<LB, LOG_N1, LOG_N1, 1>(x, 1, P.tw.fwd + limb * P.tw.stride, M);
+    } else {
+      const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
+      inv_radix<LB, LOG_N1, LOG_N1, 1, 1>(x, 1, twi, M);
+      inv_stage0<LB, LOG_N1, 1>(x, 1, twi, L, M, P.fin);
+    }
+#pragma unroll
+    for (int e = 0; e < N1; ++e) buf[e * TC + threadIdx.x] = x[0][e];
+    bulk::fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u64 *dst = (which ? P.dst1 : P.dst0) + (poly << (COL_LOG_R + LOG_N1)) + col0;
+#pragma unroll 1
+      for (int e = 0; e < N1; ++e)
+        bulk::store(dst + (static_cast<long long>(e) << COL_LOG_R), buf + e * TC, ROW_BYTES);
+      bulk::commit();
+      // refill the buffer stored one iteration ago (its reads are done once
+      // at most the group just committed is still reading)
+      if (it >= 1) {
+        const int sp = (it - 1) % S;
+        const long long tn = t - gridDim.x + static_cast<long long>(S) * gridDim.x;
+        if (tn < ntiles) {
+          bulk::wait_read<1>();
+          issue_load(tn, sp);
+        }
+      }
+    }
+  }
+  // the last tile's buffer is never refilled; drain outstanding stores
+  if (threadIdx.x == 0) bulk::wait_all();
 }
 
 // ---------------------------------------------------------------------------
