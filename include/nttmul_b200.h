@@ -248,6 +248,15 @@ int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
  */
 int nttmul_set_pipeline(int chunk_waves, int reserved);
 
+/*
+ * Schedule knob of nttmul_polymul_fused_rns for n > 4096 (process-wide):
+ * enable = 1 runs large batches (>= 4 products per group) as ONE cooperative
+ * group-persistent launch whose intermediates stay in L2; enable = 0
+ * (default, measured faster) uses the three-launch column / row / column
+ * pipeline.  Both give identical results.
+ */
+int nttmul_set_group(int enable);
+
 /* ---- measurement --------------------------------------------------------- */
 
 /*

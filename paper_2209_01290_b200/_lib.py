@@ -73,6 +73,7 @@ _PROTOS = {
     "nttmul_polymul_fused_rns_host": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                                _c_i64, _c_int, _vp, _c_i64, _vp]),
     "nttmul_set_pipeline": (_c_int, [_c_int, _c_int]),
+    "nttmul_set_group": (_c_int, [_c_int]),
     "nttmul_modmul_roof": (_c_int, [ctypes.POINTER(LimbStruct), _c_int, _c_int, _c_int,
                                     _c_i64, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
 }

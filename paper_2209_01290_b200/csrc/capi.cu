@@ -304,6 +304,75 @@ long long fused_rows_per_wave() {
 
 int g_chunk_waves = 0;  // row-kernel waves per pipeline chunk (0: no chunking; measured slower)
 
+#ifndef NTTB_GROUP
+// 1: one cooperative group-persistent launch for n > 4096 (phases == 7).
+// Measured slower than the three launches (1.13 vs 0.85 ms per cfg3 step,
+// profiles/r1/group_timing.txt): every phase already runs at the SM's
+// integer throughput, so keeping the intermediates in L2 saves nothing while
+// the column phases lose half their threads and the group barriers add waits.
+#define NTTB_GROUP 0
+#endif
+int g_group = NTTB_GROUP;
+
+// Cooperative launch of group_fused_kernel.  Returns NTTMUL_OK, or -1 when
+// the batch is too small for the group scheme (the caller falls back to the
+// three-launch pipeline).
+template <int LOG_N1, int MODE, int LB>
+int launch_group_t(u64 *c, const u64 *a, const u64 *b, u64 *ws, long long ws_words,
+                   const TwSet &tw, const LimbSet &ls, long long npolys, cudaStream_t st) {
+  using G = RowGeom<COL_LOG_R>;
+  constexpr int N1 = 1 << LOG_N1;
+  const long long n = static_cast<long long>(N1) << COL_LOG_R;
+  auto k = group_fused_kernel<LOG_N1, MODE, LB>;
+  const size_t smem = 2 * G::PADN * sizeof(u64);
+  CHECK(smem_optin(k, smem));
+  static int slots = 0;
+  static unsigned *counters[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!slots) {
+    int sms = 148, nb = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, G::T, smem) != cudaSuccess ||
+        nb < 1) {
+      cudaGetLastError();
+      nb = 1;
+    }
+    slots = nb * sms;
+  }
+  long long groups = slots / N1;
+  if (groups > ws_words / (6 * n)) groups = ws_words / (6 * n);
+  // every group should own several products, or the single-launch scheme
+  // leaves SMs idle; small batches use the three-launch pipeline
+  if (groups < 1 || npolys < 4 * (slots / N1)) return -1;
+  if (groups > 512) groups = 512;
+  if (dev < 0 || dev >= 64) return fail(NTTMUL_ECUDA, "device index %d", dev);
+  if (!counters[dev] && cudaMalloc(&counters[dev], 1024 * sizeof(unsigned)) != cudaSuccess)
+    return cuda_status("group counters");
+  if (cudaMemsetAsync(counters[dev], 0, 2 * groups * sizeof(unsigned), st) != cudaSuccess)
+    return cuda_status("group counters");
+  GroupParams P{c, a, b, ws, counters[dev], tw, ls, npolys, static_cast<int>(groups)};
+  void *args[] = {&P};
+  const cudaError_t e = cudaLaunchCooperativeKernel(
+      reinterpret_cast<const void *>(k), dim3(static_cast<unsigned>(groups * N1)), dim3(G::T),
+      args, smem, st);
+  if (e != cudaSuccess) return fail(NTTMUL_ELAUNCH, "group_fused_kernel: %s", cudaGetErrorString(e));
+  return cuda_status("group_fused_kernel");
+}
+
+template <int MODE, int LB>
+int launch_group(int log_n1, u64 *c, const u64 *a, const u64 *b, u64 *ws, long long ws_words,
+                 const TwSet &tw, const LimbSet &ls, long long npolys, cudaStream_t st) {
+  switch (log_n1) {
+    case 1: return launch_group_t<1, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
+    case 2: return launch_group_t<2, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
+    case 3: return launch_group_t<3, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
+    case 4: return launch_group_t<4, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
+    case 5: return launch_group_t<5, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
+  }
+  return -1;
+}
+
 // The fused product for n > 4096 is COL -> ROW -> COL^-1.  Unchunked, the
 // intermediates round-trip HBM (a' -> c, b' -> ws).  Chunked (default), the
 // batch is cut into pieces of `g_chunk_waves` row-kernel waves; each piece
@@ -330,6 +399,11 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
     return launch_row_fused<MODE, LB>(log_r, R, npolys, st);
   }
   const long long n = 1LL << log_n;
+  if (phases == 7 && g_group && g_chunk_waves == 0 && ls.base == 0) {
+    // workspace holds npolys * n words (the API's [B, L, n] scratch)
+    const int r = launch_group<MODE, LB>(log_n1, c, a, b, ws, npolys * n, tw, ls, npolys, st);
+    if (r != -1) return r;
+  }
   long long chunk = npolys;
   if (g_chunk_waves > 0) {
     chunk = (g_chunk_waves * fused_rows_per_wave<COL_LOG_R, MODE, LB>()) >> log_n1;
@@ -679,6 +753,12 @@ int nttmul_set_pipeline(int chunk_waves, int reserved) {
   if (chunk_waves < 0 || chunk_waves > 64 || reserved < 0)
     return fail(NTTMUL_EINVAL, "pipeline chunk_waves=%d", chunk_waves);
   g_chunk_waves = chunk_waves;
+  return NTTMUL_OK;
+}
+
+int nttmul_set_group(int enable) {
+  if (enable < 0 || enable > 1) return fail(NTTMUL_EINVAL, "set_group(%d)", enable);
+  g_group = enable;
   return NTTMUL_OK;
 }
 

@@ -805,6 +805,198 @@ __global__ void __launch_bounds__(ColPipeGeom<LOG_N1>::TC)
 }
 
 // ---------------------------------------------------------------------------
+// GROUP-PERSISTENT FUSED kernel (the fused product for n = N1 x 4096).
+//
+// The three-launch pipeline (COL -> ROW -> COL^-1) sends every intermediate
+// through HBM (72 n bytes per limb-product instead of 24 n) and runs the two
+// column launches latency-bound.  Here one cooperative launch keeps all of
+// it on chip: the resident CTAs form groups of N1; a group owns one
+// limb-product at a time and walks it through three phases separated by a
+// group barrier (release/acquire on a global counter):
+//   1. CTA i transforms column slab i (4096/N1 columns x N1 rows of a and b,
+//      read from HBM) and writes a', b' to the group's scratch;
+//   2. CTA i runs the fused row pass on row i (row stages of a, b, the
+//      Karatsuba middle and the inverse row stages) from scratch, c' over a';
+//   3. CTA i runs the inverse column stages (with the folded scale) on slab
+//      i of c' and writes c to HBM.
+// Scratch (triple-buffered per group, 3 MiB per group for n = 2^16) stays in
+// L2, and every scratch line is discarded once consumed, so HBM sees only a,
+// b (read) and c (written).  Different groups drift out of phase, so the
+// memory-bound column phases of one group overlap the integer-bound row
+// phases of the group sharing its SMs.
+
+struct GroupParams {
+  u64 *out;
+  const u64 *a;
+  const u64 *b;
+  u64 *scratch;            // groups x 3 buffers x {a', b'} x n words
+  unsigned *counters;      // two per group, zero at launch
+  TwSet tw;
+  LimbSet limbs;
+  long long npolys;
+  int groups;
+};
+
+// split group barrier: arrive (release) after a phase, wait (acquire) later,
+// so independent work can run in between
+__device__ __forceinline__ void group_arrive(unsigned *ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+  }
+}
+__device__ __forceinline__ void group_wait(unsigned *ctr, unsigned target) {
+  if (threadIdx.x == 0) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+    __threadfence();  // also invalidates this SM's L1 (scratch written elsewhere)
+  }
+  __syncthreads();
+}
+
+// scratch buffers of product number `it` of a group: {a' (then c'), b'}
+__device__ __forceinline__ u64 *group_buf(const GroupParams &P, int g, int it, long long n) {
+  return P.scratch + (static_cast<long long>(g) * 3 + it % 3) * 2 * n;
+}
+
+// phase 1: forward column stages of slab i of a and b -> a', b'
+template <int LOG_N1, int LB>
+__device__ __noinline__ void group_phase1(const GroupParams &P, long long p, int i, u64 *sa) {
+  constexpr int N1 = 1 << LOG_N1, N2 = 1 << COL_LOG_R, SW = N2 / N1;
+  constexpr long long N = static_cast<long long>(N1) * N2;
+  int limb;
+  const Limb &L = *limb_ptr(P.limbs, p, limb);
+  const Mod M = make_mod(L.q);
+  const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
+#pragma unroll 1
+  for (int j = threadIdx.x; j < 2 * SW; j += blockDim.x) {
+    const int which = j >= SW;
+    const int col = i * SW + (j - (which ? SW : 0));
+    const u64 *src = (which ? P.b : P.a) + p * N + col;
+    u64 *dst = sa + (which ? N : 0) + col;
+    u64 x[1][N1];
+#pragma unroll
+    for (int e = 0; e < N1; ++e) x[0][e] = src[static_cast<long long>(e) * N2];
+    fwd_radix<LB, LOG_N1, LOG_N1, 1>(x, 1, twf, M);
+#pragma unroll
+    for (int e = 0; e < N1; ++e) dst[static_cast<long long>(e) * N2] = x[0][e];
+  }
+}
+
+// phase 2: the fused row pass on row i of (a', b'); c' over a'
+template <int LOG_N1, int MODE, int LB>
+__device__ __noinline__ void group_phase2(const GroupParams &P, long long p, int i, u64 *sa,
+                                          u64 *sm) {
+  using G = RowGeom<COL_LOG_R>;
+  constexpr int N1 = 1 << LOG_N1, N2 = G::N2;
+  constexpr long long N = static_cast<long long>(N1) * N2;
+  int limb;
+  const Limb &L = *limb_ptr(P.limbs, p, limb);
+  const Mod M = make_mod(L.q);
+  const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
+  const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
+  const u64 rowbase = static_cast<u64>(N1) + i;
+  const long long off = static_cast<long long>(i) * N2;
+  const u64 *sb = sa + N;
+  row_prefetch<COL_LOG_R>(sm + G::PADN, sb + off);
+  cp_async_commit();
+  head_fwd<LB, COL_LOG_R, 0, G::R(0), 1, true>(sm, sa + off, nullptr, rowbase, twf, M);
+  cp_async_wait<0>();
+  __syncthreads();
+  head_fwd<LB, COL_LOG_R, 0, G::R(0), 1, false>(sm + G::PADN, nullptr, nullptr, rowbase, twf, M);
+  __syncthreads();
+  head_fwd_all<LB, COL_LOG_R, 2, 1>(sm, nullptr, nullptr, rowbase, twf, M);
+  // b' is consumed: drop its lines from L2 without a write-back
+  constexpr int LINES = N2 * 8 / 128;
+  for (int l = threadIdx.x; l < LINES; l += blockDim.x) discard_line(sb + off + l * 16);
+  tail_pass<LB, COL_LOG_R, 2, FWD_TRUNC, true, INV_SKIP, MODE>(sm, rowbase, twf, twi, L, M);
+  __syncthreads();
+  head_inv_all<LB, COL_LOG_R, G::NPASS - 1>(sm, sa + off, rowbase, twi, L, M, FIN_LAZY);
+}
+
+// phase 3: inverse column stages (+ folded scale) of slab i of c' -> c
+template <int LOG_N1, int LB>
+__device__ __noinline__ void group_phase3(const GroupParams &P, long long p, int i, u64 *sa) {
+  constexpr int N1 = 1 << LOG_N1, N2 = 1 << COL_LOG_R, SW = N2 / N1;
+  constexpr long long N = static_cast<long long>(N1) * N2;
+  int limb;
+  const Limb &L = *limb_ptr(P.limbs, p, limb);
+  const Mod M = make_mod(L.q);
+  const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
+#pragma unroll 1
+  for (int j = threadIdx.x; j < SW; j += blockDim.x) {
+    const int col = i * SW + j;
+    const u64 *src = sa + col;
+    u64 x[1][N1];
+#pragma unroll
+    for (int e = 0; e < N1; ++e) x[0][e] = src[static_cast<long long>(e) * N2];
+    inv_radix<LB, LOG_N1, LOG_N1, 1, 1>(x, 1, twi, M);
+    inv_stage0<LB, LOG_N1, 1>(x, 1, twi, L, M, FIN_SCALED_SKIP);
+    // every lane's loads have returned (their values were consumed): the
+    // 16 consecutive columns of a 128-byte line per row can be dropped
+    if ((j & 15) == 0)
+#pragma unroll
+      for (int e = 0; e < N1; ++e) discard_line(src + static_cast<long long>(e) * N2);
+    u64 *dst = P.out + p * N + col;
+#pragma unroll
+    for (int e = 0; e < N1; ++e) dst[static_cast<long long>(e) * N2] = x[0][e];
+  }
+}
+
+// Schedule per CTA (k = the group's k-th product), with split barriers so
+// independent work fills the waits:
+//   P1(0) arrive1 | for k: wait1(k) P2(k) arrive2 [P1(k+1) arrive1] wait2(k) P3(k)
+// Scratch is triple-buffered: a slow CTA may still read buffer k-1 in P3(k-1)
+// while a fast one writes buffer k+1 in P1(k+1).
+template <int LOG_N1, int MODE, int LB>
+__global__ void __launch_bounds__(RowGeom<COL_LOG_R>::T, NTTB_ROW_MINB_FUSED)
+    group_fused_kernel(const GroupParams P) {
+  constexpr int N1 = 1 << LOG_N1;
+  constexpr long long N = static_cast<long long>(N1) << COL_LOG_R;
+  extern __shared__ u64 sm[];
+  const int g = blockIdx.x / N1, i = blockIdx.x % N1;
+  if (g >= P.groups) return;
+  unsigned *ctr1 = P.counters + 2 * g, *ctr2 = ctr1 + 1;
+  unsigned t1 = 0, t2 = 0;
+  if (g < P.npolys) {
+    group_phase1<LOG_N1, LB>(P, g, i, group_buf(P, g, 0, N));
+    group_arrive(ctr1);
+    t1 += N1;
+  }
+  int k = 0;
+#ifdef NTTB_PHASE_TIMING
+#define GSTAMP(j) \
+  if (k == 4 && threadIdx.x == 0 && blockIdx.x < (1u << 16)) g_phase[blockIdx.x][j] = clock64();
+#else
+#define GSTAMP(j)
+#endif
+  for (long long p = g; p < P.npolys; p += P.groups, ++k) {
+    u64 *sa = group_buf(P, g, k, N);
+    GSTAMP(0);
+    group_wait(ctr1, t1);
+    GSTAMP(1);
+    group_phase2<LOG_N1, MODE, LB>(P, p, i, sa, sm);
+    group_arrive(ctr2);
+    GSTAMP(2);
+    t2 += N1;
+    if (p + P.groups < P.npolys) {
+      group_phase1<LOG_N1, LB>(P, p + P.groups, i, group_buf(P, g, k + 1, N));
+      group_arrive(ctr1);
+      t1 += N1;
+    }
+    GSTAMP(3);
+    group_wait(ctr2, t2);
+    GSTAMP(4);
+    group_phase3<LOG_N1, LB>(P, p, i, sa);
+    GSTAMP(5);
+  }
+#undef GSTAMP
+}
+
+// ---------------------------------------------------------------------------
 // SMALL kernel: n <= 2^12, one CTA per polynomial (per pair when fused);
 // stage loop over shared memory.  Used for n < 2^10 (the reference's unit
 // test sizes); also a schedule-independent cross-check of the row kernel.

@@ -239,6 +239,30 @@ def test_rns_cfg3_one_ciphertext(golden):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("log_n,limbs,batch", [(14, 8, 40), (16, 21, 4), (17, 32, 2)])
+def test_group_persistent_schedule(log_n, limbs, batch):
+    """The single cooperative group-persistent launch (large batches) and the
+    three-launch pipeline give identical products, equal to the oracle."""
+    basis = nt.RnsBasis.build(1 << log_n, 60, limbs, seed=0)
+    n = 1 << log_n
+    A = np.stack([np.stack([rand(q, n, 13 * b + l) for l, q in enumerate(basis.primes)])
+                  for b in range(batch)])
+    Bm = np.stack([np.stack([rand(q, n, 4099 + 13 * b + l) for l, q in enumerate(basis.primes)])
+                   for b in range(batch)])
+    lib = nt._lib
+    try:
+        lib.call("nttmul_set_group", 0)
+        three = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
+        lib.call("nttmul_set_group", 1)
+        group = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
+    finally:
+        lib.call("nttmul_set_group", 0)
+    assert np.array_equal(group, three)
+    k = 1 if log_n >= 16 else batch  # oracle on a subset at the large sizes
+    want = oracle.polymul_rns(A[:k], Bm[:k], basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(group[:k], want)
+
+
 def test_rns_host_buffers_streamed(golden):
     """Host (pinned and unpinned) [B, L, n] inputs stream through the
     chunked H2D / kernel / D2H pipeline: more chunks than device buffer sets,
