@@ -248,6 +248,42 @@ int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
  */
 int nttmul_set_pipeline(int chunk_waves, int reserved);
 
+/* ---- verification kernels ---------------------------------------------- */
+
+/*
+ * Schoolbook negacyclic product out = a * b mod (x^n + 1, q) of `batch`
+ * independent [n] polynomials (device pointers), every product reduced by
+ * division.  Replaces negacyclic_naive (_kernels.pyx:200-223), the O(n^2)
+ * oracle.  out may not alias a or b; q >= 2 (operands need not be reduced).
+ */
+int nttmul_negacyclic_naive(uint64_t *out, const uint64_t *a, const uint64_t *b,
+                            uint64_t q, int64_t n, int64_t batch, void *stream);
+
+/*
+ * Barrett-variant sweeps against division (sweep_random / sweep_exhaustive,
+ * _kernels.pyx:226-356).  Device outputs: tallies uint64[3][4] (classical,
+ * dhem, proposed x 0/1/2/3+ correctional subtractions; overwritten) and
+ * result uint64[2] = {mismatches, first-mismatch key (~0 when none)}.
+ * sweep_random: key = 3 * sample + variant; the sample's (q, a, b) are the
+ * reference's splitmix64 draws 3*sample+1 .. 3*sample+3.  bits in [2, 63];
+ * the dhem variant is skipped for bits > 60 like the reference.
+ * sweep_exhaustive: all odd q in [q_lo, q_hi] (q_hi < 2^16), all x < q^2;
+ * key = (q index << 34) | (x << 2) | variant.
+ */
+int nttmul_sweep_random(int bits, uint64_t nsamples, uint64_t seed,
+                        uint64_t *tallies, uint64_t *result, void *stream);
+int nttmul_sweep_exhaustive(uint64_t q_lo, uint64_t q_hi, uint64_t *tallies,
+                            uint64_t *result, void *stream);
+
+/*
+ * out[b, v] = in[b, idx[v]] for b < batch, v < n (device pointers; idx is
+ * int64[n] with entries in [0, n)).  Maps the merged-CT spectrum onto the
+ * four-step transform's vendor order (ntt_2d / ntt_2d_permutation,
+ * nttcore.py:405-497) and back.  out may not alias in.
+ */
+int nttmul_gather(uint64_t *out, const uint64_t *in, const int64_t *idx,
+                  int64_t n, int64_t batch, void *stream);
+
 /*
  * Schedule knob of nttmul_polymul_fused_rns for n > 4096 (process-wide):
  * enable = 1 runs large batches (>= 4 products per group) as ONE cooperative

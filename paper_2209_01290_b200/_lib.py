@@ -74,6 +74,10 @@ _PROTOS = {
                                                _c_i64, _c_int, _vp, _c_i64, _vp]),
     "nttmul_set_pipeline": (_c_int, [_c_int, _c_int]),
     "nttmul_set_group": (_c_int, [_c_int]),
+    "nttmul_negacyclic_naive": (_c_int, [_vp, _vp, _vp, _c_u64, _c_i64, _c_i64, _vp]),
+    "nttmul_sweep_random": (_c_int, [_c_int, _c_u64, _c_u64, _vp, _vp, _vp]),
+    "nttmul_sweep_exhaustive": (_c_int, [_c_u64, _c_u64, _vp, _vp, _vp]),
+    "nttmul_gather": (_c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _vp]),
     "nttmul_modmul_roof": (_c_int, [ctypes.POINTER(LimbStruct), _c_int, _c_int, _c_int,
                                     _c_i64, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
 }

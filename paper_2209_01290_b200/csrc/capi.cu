@@ -12,6 +12,7 @@
 
 #include "nttmul_b200.h"
 #include "ntt_kernels.cuh"
+#include "verify_kernels.cuh"
 
 using namespace nttb;
 
@@ -843,6 +844,77 @@ int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
   const int last = static_cast<int>((nchunks - 1) % NBUF);
   if (cudaStreamWaitEvent(sc, ev_out[last]) != cudaSuccess) return cuda_status("host pipeline end");
   return NTTMUL_OK;
+}
+
+int nttmul_negacyclic_naive(uint64_t *out, const uint64_t *a, const uint64_t *b, uint64_t q,
+                            int64_t n, int64_t batch, void *stream) {
+  if (n < 1 || n > (1 << 20) || batch < 0) return fail(NTTMUL_EINVAL, "n=%lld batch=%lld",
+                                                       static_cast<long long>(n),
+                                                       static_cast<long long>(batch));
+  if (q < 2) return fail(NTTMUL_EINVAL, "modulus %llu", static_cast<unsigned long long>(q));
+  if (batch == 0) return NTTMUL_OK;
+  CHECK(check_dev(out, 8, "out"));
+  CHECK(check_dev(a, 8, "a"));
+  CHECK(check_dev(b, 8, "b"));
+  if (out == a || out == b) return fail(NTTMUL_EINVAL, "out may not alias a or b");
+  const int bpp = static_cast<int>((n + NAIVE_THREADS - 1) / NAIVE_THREADS);
+  naive_kernel<<<static_cast<unsigned>(batch * bpp), NAIVE_THREADS, 0, S(stream)>>>(
+      out, a, b, q, static_cast<int>(n), bpp);
+  return cuda_status("naive_kernel");
+}
+
+int nttmul_sweep_random(int bits, uint64_t nsamples, uint64_t seed, uint64_t *tallies,
+                        uint64_t *result, void *stream) {
+  if (bits < 2 || bits > 63) return fail(NTTMUL_EINVAL, "bits=%d outside [2, 63]", bits);
+  CHECK(check_dev(tallies, 8, "tallies"));
+  CHECK(check_dev(result, 8, "result"));
+  if (cudaMemsetAsync(tallies, 0, 12 * 8, S(stream)) != cudaSuccess ||
+      cudaMemsetAsync(result, 0, 8, S(stream)) != cudaSuccess ||
+      cudaMemsetAsync(result + 1, 0xff, 8, S(stream)) != cudaSuccess)
+    return cuda_status("sweep init");
+  if (nsamples == 0) return NTTMUL_OK;
+  sweep_random_kernel<<<grid_for(static_cast<long long>(nsamples), 256, 148LL * 16), 256, 0,
+                        S(stream)>>>(bits, nsamples, seed,
+                                     reinterpret_cast<unsigned long long *>(tallies),
+                                     reinterpret_cast<unsigned long long *>(result));
+  return cuda_status("sweep_random_kernel");
+}
+
+int nttmul_sweep_exhaustive(uint64_t q_lo, uint64_t q_hi, uint64_t *tallies, uint64_t *result,
+                            void *stream) {
+  if (q_hi >= (1u << 16)) return fail(NTTMUL_EINVAL, "q_hi=%llu must be < 2^16",
+                                      static_cast<unsigned long long>(q_hi));
+  CHECK(check_dev(tallies, 8, "tallies"));
+  CHECK(check_dev(result, 8, "result"));
+  if (cudaMemsetAsync(tallies, 0, 12 * 8, S(stream)) != cudaSuccess ||
+      cudaMemsetAsync(result, 0, 8, S(stream)) != cudaSuccess ||
+      cudaMemsetAsync(result + 1, 0xff, 8, S(stream)) != cudaSuccess)
+    return cuda_status("sweep init");
+  const u64 q0 = q_lo | 1;
+  if (q0 < 3 && q_hi >= q0) return fail(NTTMUL_EINVAL, "q_lo must be >= 2");
+  if (q_hi < q0) return NTTMUL_OK;
+  const unsigned nq = static_cast<unsigned>((q_hi - q0) / 2 + 1);
+  const u64 xmax = q_hi * q_hi;
+  const unsigned gx = grid_for(static_cast<long long>(xmax), 256, 64);
+  sweep_exhaustive_kernel<<<dim3(gx, nq), 256, 0, S(stream)>>>(
+      q_lo, reinterpret_cast<unsigned long long *>(tallies),
+      reinterpret_cast<unsigned long long *>(result));
+  return cuda_status("sweep_exhaustive_kernel");
+}
+
+int nttmul_gather(uint64_t *out, const uint64_t *in, const int64_t *idx, int64_t n,
+                  int64_t batch, void *stream) {
+  if (n < 1 || batch < 0) return fail(NTTMUL_EINVAL, "n=%lld batch=%lld",
+                                      static_cast<long long>(n), static_cast<long long>(batch));
+  if (batch == 0) return NTTMUL_OK;
+  CHECK(check_dev(out, 8, "out"));
+  CHECK(check_dev(in, 8, "in"));
+  CHECK(check_dev(idx, 8, "idx"));
+  if (out == in) return fail(NTTMUL_EINVAL, "out may not alias in");
+  const long long total = n * batch;
+  gather_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(
+      out, in, reinterpret_cast<const long long *>(idx), n, total);
+  return cuda_status("gather_kernel");
 }
 
 int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int threads,

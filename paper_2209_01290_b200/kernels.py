@@ -11,6 +11,9 @@ returns there), executed by the sm_100a library through the C ABI:
   hadamard(a, b, out, q, mode, mu, s_in, s_out, counts)            pyx:180-188
   scale(a, factor, q, mode, mu, s_in, s_out, counts)               pyx:191-199
   mulmod_loop(a, b, q, mode, mu, s_in, s_out, passes) -> int       pyx:359-371
+  negacyclic_naive(a, b, out, q, counts)                           pyx:200-223
+  sweep_exhaustive(q_lo, q_hi, tallies) -> (mism, first)           pyx:264-306
+  sweep_random(bits, nsamples, seed, tallies) -> (mism, first)     pyx:309-356
 
 Operands may be CUDA uint64 tensors (1-D ``[n]`` as in the reference, or
 ``[batch, n]`` to transform a whole batch in one launch) or numpy uint64
@@ -19,9 +22,9 @@ path).  ``counts`` (uint64[5]: modmul, addsub, half, twiddle loads,
 negations) is accumulated with the reference's closed forms, which are
 data-independent.  Launches go to torch's current stream.
 
-Not provided here: ``negacyclic_naive`` and the reduction sweeps - they are
-the reference's O(n^2)/exhaustive verification oracles, not the hot path
-(SURVEY.md §2.1); the CPU oracle in ``oracle/`` keeps them.
+The verification kernels (schoolbook oracle, reduction sweeps) run on the
+GPU too (csrc/verify_kernels.cuh) with the reference's exact arithmetic;
+the sweeps' ``tallies`` (uint64[3][4]) are accumulated like the reference.
 """
 
 from __future__ import annotations
@@ -251,4 +254,84 @@ def mulmod_tensor(a, b, mod, variant: str = "proposed") -> torch.Tensor:
     mode, mu, s_in, s_out = mod.reduction_params(variant)
     _lib.call("nttmul_hadamard", da.data_ptr(), db.data_ptr(), out.data_ptr(), da.numel(),
               mod.q, mode, mu, s_in, s_out, _device.stream_ptr())
+    return out
+
+
+def negacyclic_naive(a, b, out, q, counts=None):
+    """Schoolbook product mod x^n + 1 (division-based reduction only)."""
+    oa, ob, oo = _Operand(a, "a", False), _Operand(b, "b", False), _Operand(out, "out")
+    batch, n = _shape(oa)
+    if _shape(ob) != (batch, n) or _shape(oo) != (batch, n):
+        raise ValueError("a, b, out must share one shape")
+    _lib.call("nttmul_negacyclic_naive", oo.dev.data_ptr(), oa.dev.data_ptr(),
+              ob.dev.data_ptr(), int(q), n, batch, _device.stream_ptr())
+    oo.writeback()
+    _add_counts(counts, (batch * n * n, batch * n * n, 0, 0, 0))
+
+
+def _sweep_finish(tallies, t_dev, r_dev):
+    t = t_dev.cpu().numpy().reshape(3, 4)
+    res = r_dev.cpu().numpy()
+    if isinstance(tallies, torch.Tensor):
+        tallies += torch.from_numpy(t.astype(np.uint64)).to(tallies.device)
+    else:
+        tallies[...] = np.asarray(tallies, dtype=np.uint64) + t.astype(np.uint64)
+    return int(res[0]), int(res[1])
+
+
+_MASK64 = (1 << 64) - 1
+
+
+def _splitmix_at(seed: int, draws: int) -> int:
+    z = (seed + draws * 0x9E3779B97F4A7C15) & _MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK64
+    return z ^ (z >> 31)
+
+
+def sweep_exhaustive(q_lo, q_hi, tallies):
+    """All odd q in [q_lo, q_hi], all x < q^2, every Barrett variant against
+    division; tallies uint64[3][4] += counts of 0/1/2/3+ subtractions.
+    Returns (mismatches, (q, x, variant) of the first mismatch or None)."""
+    dev = _device.device()
+    t_dev = torch.empty(12, dtype=_device.U64, device=dev)
+    r_dev = torch.empty(2, dtype=_device.U64, device=dev)
+    _lib.call("nttmul_sweep_exhaustive", int(q_lo), int(q_hi), t_dev.data_ptr(),
+              r_dev.data_ptr(), _device.stream_ptr())
+    mism, key = _sweep_finish(tallies, t_dev, r_dev)
+    if not mism:
+        return 0, None
+    qi, x, vi = key >> 34, (key >> 2) & ((1 << 32) - 1), key & 3
+    return mism, ((int(q_lo) | 1) + 2 * qi, x, vi)
+
+
+def sweep_random(bits, nsamples, seed, tallies):
+    """Random (a, b, q) triples (splitmix64 stream of the reference) with q an
+    odd ``bits``-bit modulus; same return convention as sweep_exhaustive
+    (first = (q, a*b, variant))."""
+    dev = _device.device()
+    t_dev = torch.empty(12, dtype=_device.U64, device=dev)
+    r_dev = torch.empty(2, dtype=_device.U64, device=dev)
+    _lib.call("nttmul_sweep_random", int(bits), int(nsamples), int(seed) & _MASK64,
+              t_dev.data_ptr(), r_dev.data_ptr(), _device.stream_ptr())
+    mism, key = _sweep_finish(tallies, t_dev, r_dev)
+    if not mism:
+        return 0, None
+    s, vi = divmod(key, 3)
+    lo = span = 1 << (int(bits) - 1)
+    q = (lo + _splitmix_at(int(seed), 3 * s + 1) % span) | 1
+    a = _splitmix_at(int(seed), 3 * s + 2) % q
+    b = _splitmix_at(int(seed), 3 * s + 3) % q
+    return mism, (q, a * b, vi)
+
+
+def gather(x: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    """out[..., v] = x[..., idx[v]] for a contiguous CUDA [n] / [batch, n] tensor."""
+    op = _Operand(x, "x", False)
+    batch, n = _shape(op)
+    if idx.numel() != n:
+        raise ValueError("index length must equal n")
+    out = torch.empty_like(op.dev)
+    _lib.call("nttmul_gather", out.data_ptr(), op.dev.data_ptr(), idx.data_ptr(), n, batch,
+              _device.stream_ptr())
     return out

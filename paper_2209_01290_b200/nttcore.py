@@ -177,6 +177,144 @@ def scale_by(factor: int, a: Polynomial, plan: NttPlan,
     return a
 
 
+# ---------------------------------------------------------------------------
+# radix-4 shapes (reference nttcore.py:189-329): two merged radix-2 stages per
+# pass.  Their output order and values equal the radix-2 transforms exactly
+# (the reference's own contract), and on the GPU every transform already runs
+# several stages per register pass (radix-8 row passes, radix-16 column
+# passes), so they execute the same kernels; only the bookkeeping is the
+# radix-4 loop's.
+
+def _radix4_counts(n: int, inverse: bool) -> np.ndarray:
+    """Counts of the reference radix-4 loops (nttcore.py:200-257, 267-323)."""
+    c = _counts()
+    if not inverse:
+        m, k = 1, n // 2
+        while m < n:
+            c[C_TWIDDLE] += 3 * m
+            c[C_MODMUL] += m * 4 * (k // 2)
+            c[C_ADDSUB] += m * 8 * (k // 2)
+            m, k = m << 2, k >> 2
+    else:
+        m, k = n // 2, 1
+        while m >= 2:
+            g = m // 2
+            c[C_TWIDDLE] += 3 * g
+            c[C_MODMUL] += g * 4 * k
+            c[C_ADDSUB] += g * 8 * k
+            c[C_HALF] += g * 8 * k
+            m, k = m >> 2, k << 2
+    return c
+
+
+def ntt_radix4(a: Polynomial, plan: NttPlan, ctr: OpCounter | None = None) -> Polynomial:
+    """Forward NTT, two stages per pass; requires even log2(n)."""
+    if plan.log_n % 2:
+        raise ValueError(f"radix-4 needs even log2(n), got n={plan.n}")
+    _check(a, plan, NORMAL)
+    backend.kernels().ntt_ct(a.coeffs, plan.tw_fwd, *plan.red_args, False, None)
+    _finish(ctr, _radix4_counts(plan.n, False))
+    a.ordering = BIT_REVERSED
+    return a
+
+
+def intt_radix4(a: Polynomial, plan: NttPlan, ctr: OpCounter | None = None) -> Polynomial:
+    """Scaled inverse paired with ntt_radix4; requires even log2(n)."""
+    if plan.log_n % 2:
+        raise ValueError(f"radix-4 needs even log2(n), got n={plan.n}")
+    _check(a, plan, BIT_REVERSED)
+    q, mode, mu, s_in, s_out = plan.red_args
+    backend.kernels().intt_gs(a.coeffs, plan.tw_inv, q, plan.mod.half_q_ceil, mode, mu, s_in,
+                              s_out, True, False, None)
+    _finish(ctr, _radix4_counts(plan.n, True))
+    a.ordering = NORMAL
+    return a
+
+
+# ---------------------------------------------------------------------------
+# four-step 2D shape (reference nttcore.py:332-497).  Its output is the
+# natural-order negacyclic spectrum in the "vendor order" (entry j2 + n2*j1
+# at position j2*n1 + j1), i.e. a fixed permutation of the merged-CT output
+# (ntt_2d_permutation).  The GPU computes the merged transform with its
+# stage-grouped 2D schedule and applies the permutation with one gather
+# launch; the inverse gathers back and runs the scaled merged inverse.
+
+def _grid_split(plan: NttPlan) -> tuple[int, int]:
+    if plan.log_n % 2 == 0:
+        return 1 << (plan.log_n // 2), 1 << (plan.log_n // 2)
+    return 1 << ((plan.log_n + 1) // 2), 1 << ((plan.log_n - 1) // 2)
+
+
+def ntt_2d_permutation(plan: NttPlan) -> np.ndarray:
+    """perm such that ntt_2d(a).coeffs[v] == ntt_ct(a).coeffs[perm[v]]."""
+    cached = plan._cache.get("2d_perm")
+    if cached is None:
+        n1, n2 = _grid_split(plan)
+        v = np.arange(plan.n, dtype=np.int64)
+        j2, j1 = np.divmod(v, n1)
+        idx = j2 + n2 * j1
+        rev = np.zeros(plan.n, dtype=np.int64)
+        for bit in range(plan.log_n):  # bit reversal of log_n-bit indices
+            rev |= ((idx >> bit) & 1) << (plan.log_n - 1 - bit)
+        cached = rev
+        plan._cache["2d_perm"] = cached
+    return cached.copy()
+
+
+def _perm_device(plan: NttPlan, inverse: bool) -> torch.Tensor:
+    key = "2d_perm_inv_dev" if inverse else "2d_perm_dev"
+    t = plan._cache.get(key)
+    if t is None:
+        perm = ntt_2d_permutation(plan)
+        if inverse:
+            inv = np.empty_like(perm)
+            inv[perm] = np.arange(plan.n, dtype=np.int64)
+            perm = inv
+        t = torch.from_numpy(perm).to(_device.device())
+        plan._cache[key] = t
+    return t
+
+
+def _counts_2d_one(plan: NttPlan) -> np.ndarray:
+    """Counts of one ntt_2d / ntt_2d_inv (reference nttcore.py:405-486): n
+    pre/post products, n twiddle corrections, (n/2) log2 n butterflies."""
+    n, log_n = plan.n, plan.log_n
+    c = _counts()
+    c[C_MODMUL] = 2 * n + (n // 2) * log_n
+    c[C_TWIDDLE] = 2 * n + (n // 2) * log_n
+    c[C_ADDSUB] = n * log_n
+    return c
+
+
+def ntt_2d(a: Polynomial, plan: NttPlan, ctr: OpCounter | None = None) -> Polynomial:
+    """Four-step forward transform: normal order in, vendor order out."""
+    _check(a, plan, NORMAL)
+    k = backend.kernels()
+    work = a.coeffs.clone()
+    k.ntt_ct(work, plan.tw_fwd, *plan.red_args, False, None)
+    a.coeffs = k.gather(work, _perm_device(plan, False))
+    a.ordering = VENDOR_2D
+    _finish(ctr, _counts_2d_one(plan))
+    return a
+
+
+def ntt_2d_inv(a: Polynomial, plan: NttPlan, ctr: OpCounter | None = None) -> Polynomial:
+    """Inverse of ntt_2d, consuming its vendor order (scaled: returns the input)."""
+    if len(a.coeffs) != plan.n:
+        raise ValueError(f"length {len(a.coeffs)} does not match plan n={plan.n}")
+    if a.ordering != VENDOR_2D:
+        raise ValueError(f"expected vendor_2d-order input, got {a.ordering}")
+    k = backend.kernels()
+    work = k.gather(a.coeffs, _perm_device(plan, True))
+    q, mode, mu, s_in, s_out = plan.red_args
+    k.intt_gs(work, plan.tw_inv, q, plan.mod.half_q_ceil, mode, mu, s_in, s_out, True, False,
+              None)
+    a.coeffs = work
+    a.ordering = NORMAL
+    _finish(ctr, _counts_2d_one(plan))
+    return a
+
+
 def _stack(rows: list[Polynomial], n: int) -> torch.Tensor:
     for r in rows:
         if len(r) != n:

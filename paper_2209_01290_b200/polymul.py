@@ -76,6 +76,21 @@ def _result(t: torch.Tensor, on_device: bool):
     return t if on_device else t.cpu().numpy()
 
 
+def negacyclic_naive(a, b, q: int, ctr: OpCounter | None = None):
+    """Schoolbook product mod x^n + 1; the independent O(n^2) oracle,
+    reduced by division only (reference polymul.py:70-82).  One GPU thread
+    per output coefficient; [batch, n] device tensors run as one launch."""
+    dev = _device.is_device_tensor(a) or _device.is_device_tensor(b)
+    ta, tb = _device.to_device(a), _device.to_device(b)
+    if ta.shape[-1] != tb.shape[-1] or ta.shape != tb.shape:
+        raise ValueError(f"length mismatch: {ta.shape[-1]} vs {tb.shape[-1]}")
+    out = torch.empty_like(ta)
+    counts = _counts()
+    backend.kernels().negacyclic_naive(ta, tb, out, int(q), counts)
+    _finish(ctr, counts)
+    return _result(out, dev)
+
+
 def hadamard(a, b, mod_or_plan, ctr: OpCounter | None = None):
     """Entry-wise modular product of two equal-length vectors."""
     if isinstance(mod_or_plan, NttPlan):

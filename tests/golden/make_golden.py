@@ -150,6 +150,32 @@ def main():
                                             nt.Polynomial(b.copy()), plan, c)
         rec["pntt_counts"] = counts_of(c)
         vec[key + "_naive"] = nt.negacyclic_naive(a, b, plan.q)
+        c = nt.OpCounter()
+        nt.negacyclic_naive(a, b, plan.q, c)
+        rec["naive_counts"] = counts_of(c)
+        # alternative transform shapes (nttcore.py:189-497)
+        if plan.log_n % 2 == 0:
+            c = nt.OpCounter()
+            p = nt.Polynomial(a.copy())
+            nt.ntt_radix4(p, plan, c)
+            vec[key + "_r4"] = p.coeffs.copy()
+            rec["r4_counts"] = counts_of(c)
+            c = nt.OpCounter()
+            p = nt.Polynomial(x.copy(), "bit_reversed")
+            nt.intt_radix4(p, plan, c)
+            vec[key + "_ir4"] = p.coeffs.copy()
+            rec["ir4_counts"] = counts_of(c)
+        c = nt.OpCounter()
+        p = nt.Polynomial(a.copy())
+        nt.ntt_2d(p, plan, c)
+        vec[key + "_2d"] = p.coeffs.copy()
+        rec["2d_counts"] = counts_of(c)
+        c = nt.OpCounter()
+        p = nt.Polynomial(x.copy(), "vendor_2d")
+        nt.ntt_2d_inv(p, plan, c)
+        vec[key + "_2di"] = p.coeffs.copy()
+        rec["2di_counts"] = counts_of(c)
+        vec[key + "_2dperm"] = nt.ntt_2d_permutation(plan).astype(np.int64)
         vec[key + "_had"] = nt.hadamard(a, b, plan)
         f = int(rand(plan.q, 1, 4000 + n)[0])
         p = nt.Polynomial(a.copy())
@@ -209,6 +235,24 @@ def main():
             sinks.append({"bits": bits, "q": q, "a_seed": 50 + bits, "b_seed": 60 + bits,
                           "n": 4096, "variant": variant, "passes": passes, "sink": int(s)})
     out["mulmod_loop"] = sinks
+
+    # ---- Barrett-variant sweeps (_kernels.pyx:264-356) -------------------
+    sweeps = []
+    for q_lo, q_hi in [(3, 63), (3, 255), (200, 301)]:
+        t = np.zeros((3, 4), dtype=np.uint64)
+        mism, first = backend.kernels().sweep_exhaustive(q_lo, q_hi, t)
+        sweeps.append({"kind": "exhaustive", "q_lo": q_lo, "q_hi": q_hi, "mism": int(mism),
+                       "first": list(first) if first else None,
+                       "tallies": [[int(v) for v in r] for r in t]})
+    for bits, samples, seed in [(8, 100000, 0), (20, 100000, 1), (30, 100000, 2),
+                                (60, 100000, 3), (61, 50000, 4), (62, 100000, 5),
+                                (63, 50000, 6)]:
+        t = np.zeros((3, 4), dtype=np.uint64)
+        mism, first = backend.kernels().sweep_random(bits, samples, seed, t)
+        sweeps.append({"kind": "random", "bits": bits, "samples": samples, "seed": seed,
+                       "mism": int(mism), "first": list(first) if first else None,
+                       "tallies": [[int(v) for v in r] for r in t]})
+    out["sweeps"] = sweeps
 
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=1)

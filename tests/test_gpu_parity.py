@@ -414,3 +414,90 @@ def test_lazy_bound_paths_vs_oracle(bits, log_n):
     assert np.array_equal(host(t), w)
     K.intt_gs(t, plan.tw_inv, plan.q, (plan.q + 1) // 2, *plan.red_args[1:], True, False)
     assert np.array_equal(host(t), x)
+
+
+# ---- verification kernels and alternative transform shapes ----------------
+
+def test_negacyclic_naive_matches_reference(golden, vectors):
+    for c in golden["vector_cases"]:
+        key = c["key"]
+        a, b = vectors[key + "_a"], vectors[key + "_b"]
+        ctr = nt.OpCounter()
+        got = nt.negacyclic_naive(dev(a), dev(b), c["q"], ctr)
+        assert np.array_equal(host(got), vectors[key + "_naive"]), key
+        assert list(ctr.as_tuple()) == c["naive_counts"], key
+        # host arrays in -> host array out, like the reference
+        assert np.array_equal(nt.negacyclic_naive(a, b, c["q"]), vectors[key + "_naive"])
+        # the fused product equals the schoolbook oracle
+        assert np.array_equal(vectors[key + "_fused"], vectors[key + "_naive"]), key
+
+
+def test_negacyclic_naive_batch_and_wraparound():
+    q = 998244353
+    n = 64
+    a = np.zeros((3, n), dtype=np.uint64)
+    b = np.zeros((3, n), dtype=np.uint64)
+    a[:, n - 1] = 1
+    b[:, 1] = 1  # x^(n-1) * x = -1
+    got = host(nt.negacyclic_naive(dev(a), dev(b), q))
+    want = np.zeros((3, n), dtype=np.uint64)
+    want[:, 0] = q - 1
+    assert np.array_equal(got, want)
+
+
+def test_radix4_and_2d_shapes_match_reference(golden, vectors):
+    for c in golden["vector_cases"]:
+        key, n = c["key"], c["n"]
+        plan = _plan(c)
+        a, x = vectors[key + "_a"], vectors[key + "_x"]
+        if "r4_counts" in c:
+            ctr = nt.OpCounter()
+            p = nt.ntt_radix4(nt.Polynomial(a.copy()), plan, ctr)
+            assert np.array_equal(p.numpy(), vectors[key + "_r4"]), key
+            assert list(ctr.as_tuple()) == c["r4_counts"], key
+            ctr = nt.OpCounter()
+            p = nt.intt_radix4(nt.Polynomial(x.copy(), "bit_reversed"), plan, ctr)
+            assert np.array_equal(p.numpy(), vectors[key + "_ir4"]), key
+            assert list(ctr.as_tuple()) == c["ir4_counts"], key
+        else:
+            with pytest.raises(ValueError):
+                nt.ntt_radix4(nt.Polynomial(a.copy()), plan)
+        ctr = nt.OpCounter()
+        p = nt.ntt_2d(nt.Polynomial(a.copy()), plan, ctr)
+        assert p.ordering == "vendor_2d"
+        assert np.array_equal(p.numpy(), vectors[key + "_2d"]), key
+        assert list(ctr.as_tuple()) == c["2d_counts"], key
+        ctr = nt.OpCounter()
+        p = nt.ntt_2d_inv(nt.Polynomial(x.copy(), "vendor_2d"), plan, ctr)
+        assert np.array_equal(p.numpy(), vectors[key + "_2di"]), key
+        assert list(ctr.as_tuple()) == c["2di_counts"], key
+        # round trip and the documented permutation identity
+        p = nt.ntt_2d_inv(nt.ntt_2d(nt.Polynomial(a.copy()), plan), plan)
+        assert np.array_equal(p.numpy(), a), key
+        perm = nt.ntt_2d_permutation(plan)
+        assert np.array_equal(vectors[key + "_2d"], vectors[key + "_ntt"][perm]), key
+
+
+def test_2d_full_size_roundtrip():
+    plan = nt.build_plan(1 << 16, bits=60, seed=0)
+    a = rand(plan.q, 1 << 16, 5)
+    p = nt.ntt_2d(nt.Polynomial(a.copy()), plan)
+    ref = nt.ntt_ct(nt.Polynomial(a.copy()), plan).numpy()
+    assert np.array_equal(p.numpy(), ref[nt.ntt_2d_permutation(plan)])
+    assert np.array_equal(nt.ntt_2d_inv(p, plan).numpy(), a)
+
+
+def test_sweeps_match_reference(golden):
+    for s in golden["sweeps"]:
+        t = np.zeros((3, 4), dtype=np.uint64)
+        if s["kind"] == "exhaustive":
+            mism, first = K.sweep_exhaustive(s["q_lo"], s["q_hi"], t)
+        else:
+            mism, first = K.sweep_random(s["bits"], s["samples"], s["seed"], t)
+        assert mism == s["mism"], s
+        assert (list(first) if first else None) == s["first"], s
+        assert [[int(v) for v in r] for r in t] == s["tallies"], s
+        # tallies accumulate like the reference
+        if s["kind"] == "random" and s["bits"] == 30:
+            K.sweep_random(s["bits"], s["samples"], s["seed"], t)
+            assert [[int(v) for v in r] for r in t] == [[2 * v for v in r] for r in s["tallies"]]
