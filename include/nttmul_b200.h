@@ -248,6 +248,31 @@ int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
  */
 int nttmul_set_pipeline(int chunk_waves, int reserved);
 
+/* ---- RNS decomposition / CRT reconstruction (rns.py:82-108) ------------- */
+
+/*
+ * Big-integer coefficients (little-endian uint64 words, words[b, j, 0..W))
+ * -> residues res[b, i, j] = c mod q_i for b < batch, j < n, i < L.
+ * word_pairs[i, w] = {2^(64 w) mod q_i, Shoup companion} (uint64[L, W, 2]).
+ * Replaces decompose (rns.py:82-91).  W <= 64 words, q_i < 2^62.
+ */
+int nttmul_crt_decompose(uint64_t *res, const uint64_t *words,
+                         const uint64_t *primes, const uint64_t *word_pairs,
+                         int num_limbs, int num_words, int64_t batch,
+                         int64_t n, void *stream);
+
+/*
+ * Residues res[b, i, j] (canonical) -> the unique words[b, j, 0..W) in
+ * [0, Q), Q = prod q_i.  inv_pairs[i] = {(Q/q_i)^-1 mod q_i, companion},
+ * m_words[i, w] = words of Q/q_i, q_words[w] = words of Q, q_recip[i] =
+ * 1.0 / q_i.  Replaces reconstruct (rns.py:94-108).
+ */
+int nttmul_crt_reconstruct(uint64_t *words, const uint64_t *res,
+                           const uint64_t *primes, const uint64_t *inv_pairs,
+                           const uint64_t *m_words, const uint64_t *q_words,
+                           const double *q_recip, int num_limbs, int num_words,
+                           int64_t batch, int64_t n, void *stream);
+
 /* ---- verification kernels ---------------------------------------------- */
 
 /*

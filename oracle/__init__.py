@@ -175,6 +175,31 @@ def polymul_rns(a: np.ndarray, b: np.ndarray, primes, psis, variant="proposed",
     return out
 
 
+# ---- RNS / CRT (reference rns.py:82-108), Python big integers -------------
+
+def crt_decompose(values, primes) -> np.ndarray:
+    """residues[i, j] = values[j] mod primes[i] (rns.py:82-91)."""
+    vals = [int(v) for v in values]
+    return np.array([[v % q for v in vals] for q in primes], dtype=np.uint64).reshape(
+        len(primes), len(vals))
+
+
+def crt_reconstruct(residues, primes) -> list[int]:
+    """The unique vector in [0, prod q) with the given residues (rns.py:94-108)."""
+    big_q = 1
+    for q in primes:
+        big_q *= int(q)
+    weights = [(big_q // int(q), pow(big_q // int(q) % int(q), -1, int(q))) for q in primes]
+    rows = [[int(x) for x in r] for r in residues]
+    out = []
+    for j in range(len(rows[0])):
+        acc = 0
+        for r, q, (quot, inv) in zip(rows, primes, weights):
+            acc += r[j] * inv % int(q) * quot
+        out.append(acc % big_q)
+    return out
+
+
 # ---- the unmodified reference (oracle/_ref) -------------------------------
 
 def reference():

@@ -78,6 +78,9 @@ _PROTOS = {
     "nttmul_sweep_random": (_c_int, [_c_int, _c_u64, _c_u64, _vp, _vp, _vp]),
     "nttmul_sweep_exhaustive": (_c_int, [_c_u64, _c_u64, _vp, _vp, _vp]),
     "nttmul_gather": (_c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _vp]),
+    "nttmul_crt_decompose": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_i64, _c_i64, _vp]),
+    "nttmul_crt_reconstruct": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                                        _c_i64, _c_i64, _vp]),
     "nttmul_modmul_roof": (_c_int, [ctypes.POINTER(LimbStruct), _c_int, _c_int, _c_int,
                                     _c_i64, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
 }

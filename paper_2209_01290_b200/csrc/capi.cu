@@ -13,6 +13,7 @@
 #include "nttmul_b200.h"
 #include "ntt_kernels.cuh"
 #include "verify_kernels.cuh"
+#include "crt_kernels.cuh"
 
 using namespace nttb;
 
@@ -915,6 +916,60 @@ int nttmul_gather(uint64_t *out, const uint64_t *in, const int64_t *idx, int64_t
   gather_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(
       out, in, reinterpret_cast<const long long *>(idx), n, total);
   return cuda_status("gather_kernel");
+}
+
+#define NTTB_CRT_WORDS(X) X(4) X(8) X(16) X(24) X(32) X(48) X(64)
+
+int nttmul_crt_decompose(uint64_t *res, const uint64_t *words, const uint64_t *primes,
+                         const uint64_t *word_pairs, int num_limbs, int num_words,
+                         int64_t batch, int64_t n, void *stream) {
+  if (num_limbs < 1 || num_words < 1 || num_words > 64 || batch < 0 || n < 1)
+    return fail(NTTMUL_EINVAL, "crt_decompose: L=%d W=%d", num_limbs, num_words);
+  if (batch == 0) return NTTMUL_OK;
+  CHECK(check_dev(res, 8, "res"));
+  CHECK(check_dev(words, 8, "words"));
+  CHECK(check_dev(primes, 8, "primes"));
+  CHECK(check_dev(word_pairs, 16, "word_pairs"));
+  const long long total = batch * n;
+  const auto *pw = reinterpret_cast<const ulonglong2 *>(word_pairs);
+  const unsigned grid = grid_for(total, 256);
+#define NTTB_DEC(WM)                                                                       \
+  if (num_words <= WM) {                                                                   \
+    crt_decompose_kernel<WM><<<grid, 256, 0, S(stream)>>>(res, words, primes, pw, num_limbs, \
+                                                          num_words, n, total);            \
+    return cuda_status("crt_decompose_kernel");                                            \
+  }
+  NTTB_CRT_WORDS(NTTB_DEC)
+#undef NTTB_DEC
+  return fail(NTTMUL_EINVAL, "num_words=%d", num_words);
+}
+
+int nttmul_crt_reconstruct(uint64_t *words, const uint64_t *res, const uint64_t *primes,
+                           const uint64_t *inv_pairs, const uint64_t *m_words,
+                           const uint64_t *q_words, const double *q_recip, int num_limbs,
+                           int num_words, int64_t batch, int64_t n, void *stream) {
+  if (num_limbs < 1 || num_words < 1 || num_words > 64 || batch < 0 || n < 1)
+    return fail(NTTMUL_EINVAL, "crt_reconstruct: L=%d W=%d", num_limbs, num_words);
+  if (batch == 0) return NTTMUL_OK;
+  CHECK(check_dev(words, 8, "words"));
+  CHECK(check_dev(res, 8, "res"));
+  CHECK(check_dev(primes, 8, "primes"));
+  CHECK(check_dev(inv_pairs, 16, "inv_pairs"));
+  CHECK(check_dev(m_words, 8, "m_words"));
+  CHECK(check_dev(q_words, 8, "q_words"));
+  CHECK(check_dev(q_recip, 8, "q_recip"));
+  const long long total = batch * n;
+  const auto *iv = reinterpret_cast<const ulonglong2 *>(inv_pairs);
+  const unsigned grid = grid_for(total, 128);
+#define NTTB_REC(WM)                                                                      \
+  if (num_words <= WM) {                                                                  \
+    crt_reconstruct_kernel<WM><<<grid, 128, 0, S(stream)>>>(                              \
+        words, res, primes, iv, m_words, q_words, q_recip, num_limbs, num_words, n, total); \
+    return cuda_status("crt_reconstruct_kernel");                                         \
+  }
+  NTTB_CRT_WORDS(NTTB_REC)
+#undef NTTB_REC
+  return fail(NTTMUL_EINVAL, "num_words=%d", num_words);
 }
 
 int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int threads,

