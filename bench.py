@@ -308,6 +308,7 @@ def main():
                "sample": sample, "parity_ct0": "bit-exact"}
 
     ntt_us = ntt_latency_us(nt, basis.plans[0]) if rank == 0 else None
+    crt = crt_rates(nt, basis, Bn) if rank == 0 else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
@@ -321,7 +322,7 @@ def main():
                        "parallelism": f"shard-by-ciphertext x{world}",
                        "l2": "inputs 2x%.0f MiB > 126 MB L2, no flush" % (A.numel() * 8 / 2**20)},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-            "ntt_us": ntt_us, "gpu_launches": args.steps * (3 if log_n1 else 1),
+            "ntt_us": ntt_us, "crt": crt, "gpu_launches": args.steps * (3 if log_n1 else 1),
             "clocks": clk.summary(), "impl": "ours",
         }
         print(json.dumps(line), flush=True)
@@ -420,6 +421,43 @@ def load_traffic(kernel: str, products: int):
     if not rec:
         return None
     return int(rec["bytes_per_product"] * products)
+
+
+def crt_rates(nt, basis, batch):
+    """RNS decomposition / CRT reconstruction of `batch` big-integer
+    polynomials (the steps either side of the product), device-resident:
+    ms per ciphertext-polynomial and the HBM bytes they move."""
+    import torch
+
+    W = nt.rns.num_words(basis)
+    n, L = basis.n, basis.num_limbs
+    g = torch.Generator(device="cuda").manual_seed(7)
+    words = torch.randint(0, 2**62, (batch, n, W), dtype=torch.int64, device="cuda",
+                          generator=g).to(torch.uint64)
+    words[:, :, W - 1] = 0  # < big_q
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            out = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps, out
+
+    dec_ms, res = timed(lambda: nt.crt_decompose(words, basis))
+    rec_ms, back = timed(lambda: nt.crt_reconstruct(res, basis))
+    assert torch.equal(back, words), "CRT round trip"
+    nbytes = batch * n * (W + L) * 8
+    return {"words_per_coeff": W, "decompose_ms_per_poly": round(dec_ms / batch, 4),
+            "reconstruct_ms_per_poly": round(rec_ms / batch, 4),
+            "decompose_gbs": round(nbytes / (dec_ms / 1e3) / 1e9, 1),
+            "reconstruct_gbs": round(nbytes / (rec_ms / 1e3) / 1e9, 1),
+            "decompose_gmodmul_s": round(batch * n * L * W / (dec_ms / 1e3) / 1e9, 1),
+            "note": f"[{batch}, {n}, {W}] words <-> [{batch}, {L}, {n}] residues, round trip exact"}
 
 
 def ntt_latency_us(nt, plan):

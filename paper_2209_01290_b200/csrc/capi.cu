@@ -918,8 +918,6 @@ int nttmul_gather(uint64_t *out, const uint64_t *in, const int64_t *idx, int64_t
   return cuda_status("gather_kernel");
 }
 
-#define NTTB_CRT_WORDS(X) X(4) X(8) X(16) X(24) X(32) X(48) X(64)
-
 int nttmul_crt_decompose(uint64_t *res, const uint64_t *words, const uint64_t *primes,
                          const uint64_t *word_pairs, int num_limbs, int num_words,
                          int64_t batch, int64_t n, void *stream) {
@@ -932,23 +930,19 @@ int nttmul_crt_decompose(uint64_t *res, const uint64_t *words, const uint64_t *p
   CHECK(check_dev(word_pairs, 16, "word_pairs"));
   const long long total = batch * n;
   const auto *pw = reinterpret_cast<const ulonglong2 *>(word_pairs);
-  const unsigned grid = grid_for(total, 256);
-#define NTTB_DEC(WM)                                                                       \
-  if (num_words <= WM) {                                                                   \
-    crt_decompose_kernel<WM><<<grid, 256, 0, S(stream)>>>(res, words, primes, pw, num_limbs, \
-                                                          num_words, n, total);            \
-    return cuda_status("crt_decompose_kernel");                                            \
-  }
-  NTTB_CRT_WORDS(NTTB_DEC)
-#undef NTTB_DEC
-  return fail(NTTMUL_EINVAL, "num_words=%d", num_words);
+  const unsigned grid = grid_for(total, CRT_THREADS);
+  const size_t smem = static_cast<size_t>(CRT_THREADS) * crt_stride(num_words) * sizeof(u64);
+  CHECK(smem_optin(crt_decompose_kernel, smem));
+  crt_decompose_kernel<<<grid, CRT_THREADS, smem, S(stream)>>>(res, words, primes, pw, num_limbs,
+                                                               num_words, n, total);
+  return cuda_status("crt_decompose_kernel");
 }
 
 int nttmul_crt_reconstruct(uint64_t *words, const uint64_t *res, const uint64_t *primes,
                            const uint64_t *inv_pairs, const uint64_t *m_words,
                            const uint64_t *q_words, const double *q_recip, int num_limbs,
                            int num_words, int64_t batch, int64_t n, void *stream) {
-  if (num_limbs < 1 || num_words < 1 || num_words > 64 || batch < 0 || n < 1)
+  if (num_limbs < 1 || num_limbs > 128 || num_words < 1 || num_words > 64 || batch < 0 || n < 1)
     return fail(NTTMUL_EINVAL, "crt_reconstruct: L=%d W=%d", num_limbs, num_words);
   if (batch == 0) return NTTMUL_OK;
   CHECK(check_dev(words, 8, "words"));
@@ -960,16 +954,13 @@ int nttmul_crt_reconstruct(uint64_t *words, const uint64_t *res, const uint64_t 
   CHECK(check_dev(q_recip, 8, "q_recip"));
   const long long total = batch * n;
   const auto *iv = reinterpret_cast<const ulonglong2 *>(inv_pairs);
-  const unsigned grid = grid_for(total, 128);
-#define NTTB_REC(WM)                                                                      \
-  if (num_words <= WM) {                                                                  \
-    crt_reconstruct_kernel<WM><<<grid, 128, 0, S(stream)>>>(                              \
-        words, res, primes, iv, m_words, q_words, q_recip, num_limbs, num_words, n, total); \
-    return cuda_status("crt_reconstruct_kernel");                                         \
-  }
-  NTTB_CRT_WORDS(NTTB_REC)
-#undef NTTB_REC
-  return fail(NTTMUL_EINVAL, "num_words=%d", num_words);
+  const unsigned grid = grid_for(total, CRT_THREADS);
+  const size_t smem =
+      static_cast<size_t>(CRT_THREADS) * (crt_stride(num_words) + num_limbs) * sizeof(u64);
+  CHECK(smem_optin(crt_reconstruct_kernel, smem));
+  crt_reconstruct_kernel<<<grid, CRT_THREADS, smem, S(stream)>>>(
+      words, res, primes, iv, m_words, q_words, q_recip, num_limbs, num_words, n, total);
+  return cuda_status("crt_reconstruct_kernel");
 }
 
 int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int threads,

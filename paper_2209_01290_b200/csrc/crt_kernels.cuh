@@ -20,126 +20,152 @@
 
 namespace nttb {
 
+// A block's coefficients are CRT_THREADS consecutive rows of W words: they
+// move between HBM and shared memory with coalesced accesses, and each thread
+// reads / writes its own row from shared memory with an odd word stride
+// (conflict-free 8-byte accesses).
+constexpr int CRT_THREADS = 128;
+constexpr int CRT_ILP = 4;  // limbs per decompose pass
+__host__ __device__ constexpr int crt_stride(int W) { return W | 1; }
+
 // ---- decompose: one thread per coefficient, all limbs ----------------------
-template <int WMAX>
-__global__ void __launch_bounds__(256)
+// The thread's words stay in its shared-memory row (no register arrays, so
+// any W works without local memory).
+__global__ void __launch_bounds__(CRT_THREADS)
     crt_decompose_kernel(u64 *__restrict__ res, const u64 *__restrict__ words,
                          const u64 *__restrict__ qs, const ulonglong2 *__restrict__ pw,
                          int L, int W, long long n, long long total) {
-  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+  extern __shared__ u64 cw[];
+  const int S = crt_stride(W);
+  for (long long t0 = blockIdx.x * static_cast<long long>(CRT_THREADS); t0 < total;
+       t0 += static_cast<long long>(gridDim.x) * CRT_THREADS) {
+    const int rows = total - t0 < CRT_THREADS ? static_cast<int>(total - t0) : CRT_THREADS;
+    __syncthreads();
+    for (int k = threadIdx.x; k < rows * W; k += CRT_THREADS)
+      cw[(k / W) * S + k % W] = words[t0 * W + k];
+    __syncthreads();
+    if (threadIdx.x >= rows) continue;
+    const long long t = t0 + threadIdx.x;
     const long long b = t / n, j = t - b * n;
-    u64 c[WMAX];
+    const u64 *row = cw + threadIdx.x * S;
+    // CRT_ILP limbs at a time: independent accumulator chains share each
+    // word read from shared memory
+    for (int i0 = 0; i0 < L; i0 += CRT_ILP) {
+      Mod M[CRT_ILP];
+      u64 acc[CRT_ILP];
 #pragma unroll
-    for (int w = 0; w < WMAX; ++w) c[w] = w < W ? words[t * W + w] : 0;
-    for (int i = 0; i < L; ++i) {
-      const u64 q = qs[i];
-      const Mod M = make_mod(q);
-      u64 acc = 0;
+      for (int u = 0; u < CRT_ILP; ++u) {
+        M[u] = make_mod(qs[i0 + u < L ? i0 + u : i0]);
+        acc[u] = 0;
+      }
+#pragma unroll 2
+      for (int w = 0; w < W; ++w) {
+        const u64 c = row[w];
 #pragma unroll
-      for (int w = 0; w < WMAX; ++w) {
-        if (w < W) {
-          const ulonglong2 p = pw[i * W + w];
-          const u64 r = csub(csub(shoup4(c[w], p.x, p.y, M), M.q2), q);  // [0, q)
-          acc = csub(acc + r, q);
+        for (int u = 0; u < CRT_ILP; ++u) {
+          const int i = i0 + u < L ? i0 + u : i0;
+          const ulonglong2 p = pw[static_cast<long long>(i) * W + w];
+          const u64 r = csub(csub(shoup4(c, p.x, p.y, M[u]), M[u].q2), M[u].q);  // [0, q)
+          acc[u] = csub(acc[u] + r, M[u].q);
         }
       }
-      res[(b * L + i) * n + j] = acc;
+#pragma unroll
+      for (int u = 0; u < CRT_ILP; ++u)
+        if (i0 + u < L) res[(b * L + i0 + u) * n + j] = acc[u];
     }
   }
 }
 
 // ---- reconstruct: one thread per coefficient -------------------------------
-template <int WMAX>
-__global__ void __launch_bounds__(128)
+// sum_i y_i M_i is formed column by column (word w from the low halves of
+// y_i M_i[w] plus the high halves of column w-1 and the carry), straight
+// into the thread's shared-memory row; then k Q is subtracted and one
+// correction applied on that row.  y_i live in shared memory too.
+__global__ void __launch_bounds__(CRT_THREADS)
     crt_reconstruct_kernel(u64 *__restrict__ words, const u64 *__restrict__ res,
                            const u64 *__restrict__ qs, const ulonglong2 *__restrict__ inv,
                            const u64 *__restrict__ mw, const u64 *__restrict__ bigq,
                            const double *__restrict__ qrecip, int L, int W, long long n,
                            long long total) {
   typedef unsigned __int128 u128;
-  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long b = t / n, j = t - b * n;
-    u64 acc[WMAX + 1];
-#pragma unroll
-    for (int w = 0; w <= WMAX; ++w) acc[w] = 0;
-    double frac = 0.0;
-    for (int i = 0; i < L; ++i) {
-      const u64 q = qs[i];
-      const Mod M = make_mod(q);
-      const ulonglong2 iv = inv[i];
-      const u64 y = shoup(res[(b * L + i) * n + j], iv.x, iv.y, M);  // canonical
-      frac += static_cast<double>(y) * qrecip[i];
-      u64 carry = 0;
-#pragma unroll
-      for (int w = 0; w < WMAX; ++w) {
-        if (w < W) {
-          const u128 s = static_cast<u128>(y) * mw[i * W + w] + acc[w] + carry;
-          acc[w] = static_cast<u64>(s);
-          carry = static_cast<u64>(s >> 64);
-        }
+  extern __shared__ u64 cw[];
+  const int S = crt_stride(W);
+  u64 *ys = cw + CRT_THREADS * S;  // [L][CRT_THREADS]
+  for (long long t0 = blockIdx.x * static_cast<long long>(CRT_THREADS); t0 < total;
+       t0 += static_cast<long long>(gridDim.x) * CRT_THREADS) {
+    const int rows = total - t0 < CRT_THREADS ? static_cast<int>(total - t0) : CRT_THREADS;
+    __syncthreads();  // the previous tile's rows have been stored
+    if (threadIdx.x < rows) {
+      const long long t = t0 + threadIdx.x;
+      const long long b = t / n, j = t - b * n;
+      double frac = 0.0;
+      for (int i = 0; i < L; ++i) {
+        const u64 q = qs[i];
+        const Mod M = make_mod(q);
+        const ulonglong2 iv = inv[i];
+        const u64 y = shoup(res[(b * L + i) * n + j], iv.x, iv.y, M);  // canonical
+        ys[i * CRT_THREADS + threadIdx.x] = y;
+        frac += static_cast<double>(y) * qrecip[i];
       }
-#pragma unroll
-      for (int w = 0; w < WMAX; ++w)
-        if (w == W) acc[w] += carry;  // top word (sum < L Q < 2^(64 W + 64))
-      if (W == WMAX) acc[WMAX] += carry;
-    }
-    // acc -= k Q with k = floor(frac), then one correction either way
-    const u64 k = static_cast<u64>(floor(frac));
-    u64 borrow = 0, kc = 0;
-#pragma unroll
-    for (int w = 0; w <= WMAX; ++w) {
-      if (w <= W) {
-        const u128 kq = static_cast<u128>(k) * (w < W ? bigq[w] : 0) + kc;
+      const u64 k = static_cast<u64>(floor(frac));  // exact or off by one
+      u64 *row = cw + threadIdx.x * S;
+      // column sums: word w = lo(col), carry = hi(col); the top word (< L)
+      // is kept in `top`
+      u128 carry = 0, hsum = 0;
+      for (int w = 0; w < W; ++w) {
+        u128 col = carry + hsum;
+        u128 hnext = 0;
+        for (int i = 0; i < L; ++i) {
+          const u128 p = static_cast<u128>(ys[i * CRT_THREADS + threadIdx.x]) * mw[i * W + w];
+          col += static_cast<u64>(p);
+          hnext += static_cast<u64>(p >> 64);
+        }
+        row[w] = static_cast<u64>(col);
+        carry = col >> 64;
+        hsum = hnext;
+      }
+      u64 top = static_cast<u64>(carry + hsum);
+      // row -= k Q
+      u64 borrow = 0, kc = 0;
+      for (int w = 0; w < W; ++w) {
+        const u128 kq = static_cast<u128>(k) * bigq[w] + kc;
         kc = static_cast<u64>(kq >> 64);
-        const u64 sub = static_cast<u64>(kq);
-        const u64 a = acc[w];
-        const u64 d = a - sub - borrow;
+        const u64 sub = static_cast<u64>(kq), a = row[w];
+        row[w] = a - sub - borrow;
         borrow = (a < sub) || (a - sub < borrow) ? 1 : 0;
-        acc[w] = d;
       }
-    }
-    // top word (index W): ~0 after an over-subtraction (k one too large),
-    // 1 or 0 otherwise (k exact or one too small)
-    u64 top = 0;
-#pragma unroll
-    for (int w = 0; w <= WMAX; ++w)
-      if (w == W) top = acc[w];
-    if (top == ~0ULL) {  // negative: add Q back
-      u64 c = 0;
-#pragma unroll
-      for (int w = 0; w < WMAX; ++w) {
-        if (w < W) {
-          const u128 s = static_cast<u128>(acc[w]) + bigq[w] + c;
-          acc[w] = static_cast<u64>(s);
-          c = static_cast<u64>(s >> 64);
+      top = top - kc - borrow;
+      if (top == ~0ULL) {  // k was one too large: add Q back
+        u64 c = 0;
+        for (int w = 0; w < W; ++w) {
+          const u128 s2 = static_cast<u128>(row[w]) + bigq[w] + c;
+          row[w] = static_cast<u64>(s2);
+          c = static_cast<u64>(s2 >> 64);
         }
-      }
-    } else {  // subtract Q once more if acc >= Q
-      int ge = top != 0 ? 2 : 1;  // compare from the top word down
-#pragma unroll
-      for (int w = WMAX - 1; w >= 0; --w) {
-        if (w < W && ge == 1) {
-          if (acc[w] > bigq[w]) ge = 2;
-          else if (acc[w] < bigq[w]) ge = 0;
+      } else {  // k exact or one too small: subtract Q once if row >= Q
+        bool ge = top != 0;
+        if (!ge) {
+          ge = true;  // equal counts as >=
+          for (int w = W - 1; w >= 0; --w) {
+            if (row[w] != bigq[w]) {
+              ge = row[w] > bigq[w];
+              break;
+            }
+          }
         }
-      }
-      if (ge) {
-        u64 br = 0;
-#pragma unroll
-        for (int w = 0; w < WMAX; ++w) {
-          if (w < W) {
-            const u64 a = acc[w], s = bigq[w];
-            acc[w] = a - s - br;
-            br = (a < s) || (a - s < br) ? 1 : 0;
+        if (ge) {
+          u64 br = 0;
+          for (int w = 0; w < W; ++w) {
+            const u64 a = row[w], s2 = bigq[w];
+            row[w] = a - s2 - br;
+            br = (a < s2) || (a - s2 < br) ? 1 : 0;
           }
         }
       }
     }
-#pragma unroll
-    for (int w = 0; w < WMAX; ++w)
-      if (w < W) words[t * W + w] = acc[w];
+    __syncthreads();
+    for (int k = threadIdx.x; k < rows * W; k += CRT_THREADS)
+      words[t0 * W + k] = cw[(k / W) * S + k % W];
   }
 }
 
