@@ -556,3 +556,33 @@ def test_polymul_rns_words_cfg3_residue_consistency(golden):
     assert np.array_equal(rc[:1], want)
     # every output coefficient is the canonical representative (< big_q)
     assert max(nt.words_to_ints(host(Cw[1])[:512])) < basis.big_q
+
+
+# ---- verification suites (reference verify.py / test_acceptance.py) -------
+
+def test_acceptance_reduction_criteria():
+    """Criteria 1-4 of the reference acceptance gate on the GPU sweeps:
+    exhaustive q in [3, 255], 10^6 random samples per bit size, subtraction
+    bounds, classical second-subtraction frequency."""
+    V = nt.verify
+    t = np.zeros((3, 4), dtype=np.uint64)
+    r = V.reduction_exhaustive(3, 255, t)
+    assert r.passed, r.line()
+    for bits in (28, 29, 30, 62):
+        t = np.zeros((3, 4), dtype=np.uint64)
+        r = V.reduction_random(bits, 1_000_000, 42, t)
+        assert r.passed, r.line()
+        if bits == 30:
+            frac = r.measurements["classical_two_sub_fraction"]
+            assert 0 < frac < 0.05
+    # a failing configuration is reported with the reference's message shape
+    r = V.reduction_random(63, 1000, 6)
+    assert not r.passed and "mismatches; first: proposed(" in r.detail
+
+
+def test_verify_suites_pass():
+    res = nt.verify.run_all(samples=1000)
+    assert [x.status for x in res] == ["PASS"] * len(res), [x.line() for x in res]
+    names = [x.name for x in res]
+    assert names[0] == "reduction-exhaustive q in [3, 255]"
+    assert "polymul-three-way x100" in names and "rns-roundtrip x20" in names
