@@ -244,6 +244,33 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
   }
 }
 
+// Barrier between two row passes.  A pass with first stage S0 transforms
+// independent blocks of 2^(LOG_R - S0) elements; when every pass gives each
+// thread one unit (R == LOG_E), the threads that own a block are the
+// 2^(LOG_R - S0 - LOG_E) consecutive threads tid / that-many, in the passes
+// on both sides of the barrier (pass blocks nest, and the tail's 8-element
+// units sit inside the last pass's blocks).  So only those threads need to
+// meet: a warp-level sync for blocks of <= 32 threads, a named barrier for
+// blocks of 64..T/2 threads, the CTA barrier only for whole-row blocks.
+#ifndef NTTB_LOCAL_SYNC
+#define NTTB_LOCAL_SYNC 1
+#endif
+template <int LOG_R, int S0_BLOCK>
+__device__ __forceinline__ void row_sync() {
+  using G = RowGeom<LOG_R>;
+  constexpr bool ONE_UNIT = G::HEAD % G::NPASS == 0 && G::HEAD / G::NPASS == NTTB_ROW_LOG_E;
+  constexpr int THREADS = 1 << (LOG_R - S0_BLOCK - NTTB_ROW_LOG_E);
+  if constexpr (!NTTB_LOCAL_SYNC || !ONE_UNIT || THREADS >= G::T) {
+    __syncthreads();
+  } else if constexpr (THREADS <= 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + static_cast<int>(threadIdx.x) / THREADS),
+                 "n"(THREADS)
+                 : "memory");
+  }
+}
+
 // all forward head passes, pass i = 0 .. NPASS-1 (pass 0 reads global)
 template <int LB, int LOG_R, int NP, int I = 0>
 __device__ __forceinline__ void head_fwd_all(u64 *sm, const u64 *g0, const u64 *g1,
@@ -252,7 +279,7 @@ __device__ __forceinline__ void head_fwd_all(u64 *sm, const u64 *g0, const u64 *
   using G = RowGeom<LOG_R>;
   if constexpr (I < G::NPASS) {
     head_fwd<LB, LOG_R, G::S0(I), G::R(I), NP, I == 0>(sm, g0, g1, rowbase, tw, M);
-    __syncthreads();
+    row_sync<LOG_R, G::S0(I)>();
     if (I == 0) NTTB_STAMP(1);
     head_fwd_all<LB, LOG_R, NP, I + 1>(sm, g0, g1, rowbase, tw, M);
   }
@@ -267,7 +294,7 @@ __device__ __forceinline__ void head_inv_all(u64 *sm, u64 *gout, u64 rowbase,
   if constexpr (I > 0) {
     head_inv<LB, LOG_R, G::S0(I), G::R(I), false>(sm, nullptr, rowbase, tw, L, M,
                                                   FIN_LAZY);
-    __syncthreads();
+    row_sync<LOG_R, G::S0(I - 1)>();
     head_inv_all<LB, LOG_R, I - 1>(sm, gout, rowbase, tw, L, M, fin);
   } else {
     head_inv<LB, LOG_R, 0, G::R(0), true>(sm, gout, rowbase, tw, L, M, fin);
@@ -486,12 +513,14 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
   }
   NTTB_STAMP(2);
   tail_pass<LB, LOG_R, NP, FWD, MID, INV, MODE>(sm, rowbase, twf, twi, L, M);
-  __syncthreads();
+  if (INV != INV_NONE || MID)
+    row_sync<LOG_R, G::S0(G::NPASS - 1)>();  // the inverse passes read back this tail
+  else
+    __syncthreads();  // the plain store below reads the whole row
   NTTB_STAMP(3);
   if (INV != INV_NONE || MID) {
     head_inv_all<LB, LOG_R, G::NPASS - 1>(sm, P.out + off, rowbase, twi, L, M,
                                           P.log_n1 == 0 ? P.fin : FIN_LAZY);
-    __syncthreads();
     NTTB_STAMP(4);
   } else {
 #pragma unroll 4
@@ -567,14 +596,18 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T, NTTB_ROW_MINB_FUSED)
 #define NTTB_COL_LOG_R 12
 #endif
 #ifndef NTTB_COL_VEC
-#define NTTB_COL_VEC 2
+#define NTTB_COL_VEC 1
 #endif
 #ifndef NTTB_COL_MINB
 #define NTTB_COL_MINB 2
 #endif
+#ifndef NTTB_COL_MINB_INV
+#define NTTB_COL_MINB_INV 4
+#endif
 constexpr int COL_LOG_R = NTTB_COL_LOG_R;  // row length used for n > 2^COL_LOG_R
 constexpr int COL_THREADS = 256;
 constexpr int COL_VEC = NTTB_COL_VEC;      // adjacent columns per thread (1 or 2)
+static_assert(COL_VEC == 1 || COL_VEC == 2, "column vector width");
 
 struct ColParams {
   const u64 *src0;
@@ -592,10 +625,20 @@ struct ColParams {
 // Each thread owns COL_VEC adjacent columns (one 8*COL_VEC-byte vector per
 // row, coalesced across the warp) and runs all LOG_N1 column stages on them
 // in registers; the stages' twiddles tw[1 .. N1) are uniform across the grid.
+// Per-direction geometry (measured, sweep_r26): the forward pass (two
+// sources, 4 stages) runs one column per thread with up to 128 registers;
+// the inverse pass (one source + folded scale) one column per thread at 4
+// CTAs per SM (64 registers).
+template <bool INV>
+struct ColGeom {
+  static constexpr int V = NTTB_COL_VEC;
+  static constexpr int MINB = INV ? NTTB_COL_MINB_INV : NTTB_COL_MINB;
+};
+
 template <int LOG_N1, bool INV, int LB>
-__global__ void __launch_bounds__(COL_THREADS, NTTB_COL_MINB) col_kernel(const ColParams P) {
+__global__ void __launch_bounds__(COL_THREADS, ColGeom<INV>::MINB) col_kernel(const ColParams P) {
   constexpr int N1 = 1 << LOG_N1;
-  constexpr int V = COL_VEC;
+  constexpr int V = ColGeom<INV>::V;
   const long long vecs = (P.npolys << COL_LOG_R) / V;  // column vectors per source
   const long long gid = blockIdx.x * static_cast<long long>(COL_THREADS) +
                         threadIdx.x;
@@ -913,7 +956,7 @@ __device__ __noinline__ void group_phase2(const GroupParams &P, long long p, int
   constexpr int LINES = N2 * 8 / 128;
   for (int l = threadIdx.x; l < LINES; l += blockDim.x) discard_line(sb + off + l * 16);
   tail_pass<LB, COL_LOG_R, 2, FWD_TRUNC, true, INV_SKIP, MODE>(sm, rowbase, twf, twi, L, M);
-  __syncthreads();
+  row_sync<COL_LOG_R, G::S0(G::NPASS - 1)>();
   head_inv_all<LB, COL_LOG_R, G::NPASS - 1>(sm, sa + off, rowbase, twi, L, M, FIN_LAZY);
 }
 
