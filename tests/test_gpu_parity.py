@@ -586,3 +586,34 @@ def test_verify_suites_pass():
     names = [x.name for x in res]
     assert names[0] == "reduction-exhaustive q in [3, 255]"
     assert "polymul-three-way x100" in names and "rns-roundtrip x20" in names
+
+
+@pytest.mark.parametrize("log_n,limbs,batch", [(14, 8, 64), (17, 32, 8)])
+def test_baseline_configs_full_batch(log_n, limbs, batch):
+    """BASELINE cfg2 (N=2^14, 8 limbs, 64 products) and cfg4 (N=2^17, 32
+    limbs, 8 ciphertexts) at full size: first and last ciphertext against the
+    oracle, and bilinearity c(a, b1 + b2) = c(a, b1) + c(a, b2) mod q over the
+    whole batch (a size-independent check of every product)."""
+    basis = nt.RnsBasis.build(1 << log_n, 60, limbs, seed=0)
+    n = 1 << log_n
+    q = torch.tensor(np.array(basis.primes, dtype=np.uint64).astype(np.int64),
+                     device="cuda").view(1, limbs, 1)
+    g = torch.Generator(device="cuda").manual_seed(log_n)
+
+    def rnd():
+        x = torch.randint(0, 2**62, (batch, limbs, n), dtype=torch.int64, device="cuda",
+                          generator=g)
+        return (x % q).to(torch.uint64)
+
+    A, B1, B2 = rnd(), rnd(), rnd()
+    B12 = ((B1.to(torch.int64) + B2.to(torch.int64)) % q).to(torch.uint64)
+    C1 = nt.polymul_rns_batch(A, B1, basis)
+    C2 = nt.polymul_rns_batch(A, B2, basis)
+    C12 = nt.polymul_rns_batch(A, B12, basis)
+    # (C1 + C2) mod q, in int64 without overflow (values < 2^60)
+    S = ((C1.to(torch.int64) + C2.to(torch.int64)) % q).to(torch.uint64)
+    assert torch.equal(S, C12)
+    psis = [p.psi for p in basis.plans]
+    for i in (0, batch - 1):
+        want = oracle.polymul_rns(host(A[i:i + 1]), host(B1[i:i + 1]), basis.primes, psis)
+        assert np.array_equal(host(C1[i:i + 1]), want), i
