@@ -127,11 +127,11 @@ int launch_row_m(int log_r, const RowParams &P, long long rows, cudaStream_t st)
 
 // ---- persistent fused row kernel -------------------------------------------
 #ifndef NTTB_PERSISTENT
-#define NTTB_PERSISTENT 0  // measured slower: 3 row buffers leave L1 no room for twiddles
+#define NTTB_PERSISTENT 0  // 1: pipelined persistent fused row kernel (measured 0.622 vs 0.572 ms, sweep_r29)
 #endif
 template <int LOG_R, int MODE, int LB>
 int launch_row_persistent_t(const RowParams &P, long long rows, cudaStream_t st) {
-  const size_t smem = 3 * RowGeom<LOG_R>::PADN * sizeof(u64);
+  const size_t smem = 2 * RowGeom<LOG_R>::PADN * sizeof(u64);
   auto k = row_fused_persistent<LOG_R, MODE, LB>;
   CHECK(smem_optin(k, smem));
   static int slots = 0;  // resident CTAs per device for this instantiation
@@ -153,16 +153,11 @@ int launch_row_persistent_t(const RowParams &P, long long rows, cudaStream_t st)
 
 template <int MODE, int LB>
 int launch_row_fused(int log_r, const RowParams &P, long long rows, cudaStream_t st) {
-#if NTTB_PERSISTENT
-  switch (log_r) {
-    case 10: return launch_row_persistent_t<10, MODE, LB>(P, rows, st);
-    case 11: return launch_row_persistent_t<11, MODE, LB>(P, rows, st);
-    case 12: return launch_row_persistent_t<12, MODE, LB>(P, rows, st);
-  }
-  return fail(NTTMUL_EINVAL, "row size 2^%d unsupported", log_r);
-#else
+  // the pipelined persistent kernel for the 4096-word rows of n > 4096
+  // (pipeline chunking, with its scratch discards, keeps the plain kernel)
+  if (NTTB_PERSISTENT && log_r == 12 && !P.discard_in)
+    return launch_row_persistent_t<12, MODE, LB>(P, rows, st);
   return launch_row_m<FWD_TRUNC, true, INV_SKIP, MODE, LB>(log_r, P, rows, st);
-#endif
 }
 
 // ---- column kernel dispatch -------------------------------------------------

@@ -529,61 +529,78 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
 }
 
 // ---------------------------------------------------------------------------
-// PERSISTENT fused row kernel.  One CTA per (SM x resident slot) walks rows
-// gridDim.x apart.  Row inputs arrive by cp.async (LDGSTS) straight into
-// shared memory: b of the current row streams in while a's first pass runs,
-// and a of the NEXT row streams into a third buffer during the whole current
-// row - so the HBM latency that dominated the first pass is hidden.
+// PERSISTENT fused row kernel with a software-pipelined input stream.
+//
+// One CTA per resident slot walks rows gridDim.x apart.  The next row's
+// inputs are copied (cp.async) into the SAME two buffers as soon as each
+// becomes free, so no extra shared memory is needed: b's buffer is free once
+// the tail has consumed b (its copy is issued before the last inverse pass),
+// a's buffer once the last inverse pass has read it (its copy is issued at
+// the end of the row).  The next row then starts with b's first pass (data
+// already landed) while a's copy completes.  In the one-row-per-CTA kernel
+// both CTAs of an SM start together and wait on HBM together; here that
+// latency hides behind the previous row's last pass.
+
+// inverse head passes I .. 1, each followed by its barrier (the one after
+// pass 1 is the whole-row barrier before pass 0)
+template <int LB, int LOG_R, int I>
+__device__ __forceinline__ void head_inv_to1(u64 *sm, u64 rowbase, const ulonglong2 *tw,
+                                             const Limb &L, const Mod &M) {
+  using G = RowGeom<LOG_R>;
+  if constexpr (I > 0) {
+    head_inv<LB, LOG_R, G::S0(I), G::R(I), false>(sm, nullptr, rowbase, tw, L, M, FIN_LAZY);
+    row_sync<LOG_R, G::S0(I - 1)>();
+    head_inv_to1<LB, LOG_R, I - 1>(sm, rowbase, tw, L, M);
+  }
+}
 
 template <int LOG_R, int MODE, int LB>
 __global__ void __launch_bounds__(RowGeom<LOG_R>::T, NTTB_ROW_MINB_FUSED)
     row_fused_persistent(const RowParams P, long long nrows) {
   using G = RowGeom<LOG_R>;
-  extern __shared__ u64 smp[];
-  u64 *const bufB = smp + G::PADN;  // a alternates between smp and smp + 2 PADN
+  extern __shared__ u64 sm[];
+  u64 *const sa = sm, *const sb = sm + G::PADN;
   long long row = blockIdx.x;
-  if (row < nrows) row_prefetch<LOG_R>(smp, P.in0 + row * G::N2);
-  cp_async_commit();
-  for (int it = 0; row < nrows; row += gridDim.x, ++it) {
-    u64 *const sa = smp + ((it & 1) ? 2 * G::PADN : 0);
+  if (row < nrows) {
+    row_prefetch<LOG_R>(sb, P.in1 + row * G::N2);
+    cp_async_commit();
+    row_prefetch<LOG_R>(sa, P.in0 + row * G::N2);
+    cp_async_commit();
+  }
+  for (; row < nrows; row += gridDim.x) {
     const long long poly = row >> P.log_n1;
     const int r = static_cast<int>(row & ((1LL << P.log_n1) - 1));
     int limb;
-    const Limb L = get_limb(P.limbs, poly, limb);
+    const Limb &L = *limb_ptr(P.limbs, poly, limb);
     const Mod M = make_mod(L.q);
     const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
     const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
     const u64 rowbase = (1ULL << P.log_n1) + r;
     const long long off = row * G::N2;
-    NTTB_STAMP(0);
-    // b of this row, then a of the next row (always commit: uniform counting)
-    row_prefetch<LOG_R>(bufB, P.in1 + off);
-    cp_async_commit();
     const long long next = row + gridDim.x;
-    if (next < nrows)
-      row_prefetch<LOG_R>(smp + ((it & 1) ? 0 : 2 * G::PADN), P.in0 + next * G::N2);
-    cp_async_commit();
-    cp_async_wait<2>();  // a(row) landed
+    NTTB_STAMP(0);
+    cp_async_wait<1>();  // b(row) has landed; a(row) may still be in flight
     __syncthreads();
-    // head passes: a from its buffer, then b once it has landed.  The two
-    // polynomials use different smem slots, so pass them separately.
-    head_fwd_all_smem<LB, LOG_R>(sa, rowbase, twf, M);
-    cp_async_wait<1>();  // b(row) landed
+    head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sb, nullptr, nullptr, rowbase, twf, M);
+    cp_async_wait<0>();  // a(row)
+    __syncthreads();
+    head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sa, nullptr, nullptr, rowbase, twf, M);
     __syncthreads();
     NTTB_STAMP(1);
-    head_fwd_all_smem<LB, LOG_R>(bufB, rowbase, twf, M);
-    if (P.discard_in) {
-      constexpr int LINES = G::N2 * 8 / 128;
-      for (int i = threadIdx.x; i < 2 * LINES; i += G::T)
-        discard_line((i < LINES ? P.in0 : P.in1) + off + (i % LINES) * 16);
-    }
+    head_fwd_all<LB, LOG_R, 2, 1>(sm, nullptr, nullptr, rowbase, twf, M);
     NTTB_STAMP(2);
-    tail_pass_split<LB, LOG_R, MODE>(sa, bufB, rowbase, twf, twi, L, M);
-    __syncthreads();
+    tail_pass<LB, LOG_R, 2, FWD_TRUNC, true, INV_SKIP, MODE>(sm, rowbase, twf, twi, L, M);
+    row_sync<LOG_R, G::S0(G::NPASS - 1)>();
     NTTB_STAMP(3);
-    head_inv_all<LB, LOG_R, G::NPASS - 1>(sa, P.out + off, rowbase, twi, L, M,
+    head_inv_to1<LB, LOG_R, G::NPASS - 1>(sm, rowbase, twi, L, M);
+    // whole-row barrier passed: b is dead, refill its buffer with b(next)
+    if (next < nrows) row_prefetch<LOG_R>(sb, P.in1 + next * G::N2);
+    cp_async_commit();
+    head_inv<LB, LOG_R, 0, G::R(0), true>(sa, P.out + off, rowbase, twi, L, M,
                                           P.log_n1 == 0 ? P.fin : FIN_LAZY);
-    __syncthreads();  // sa / bufB free before the next row's copies land there
+    __syncthreads();  // every thread has read a's buffer
+    if (next < nrows) row_prefetch<LOG_R>(sa, P.in0 + next * G::N2);
+    cp_async_commit();
     NTTB_STAMP(4);
   }
   cp_async_wait<0>();
