@@ -322,7 +322,7 @@ def main():
                        "parallelism": f"shard-by-ciphertext x{world}",
                        "l2": "inputs 2x%.0f MiB > 126 MB L2, no flush" % (A.numel() * 8 / 2**20)},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-            "ntt_us": ntt_us, "crt": crt, "gpu_launches": args.steps * (3 if log_n1 else 1),
+            "ntt_us": ntt_us, "crt": crt, "gpu_launches": args.steps * (3 if log_n1 else 1) * (2 if log_n1 and Bn * L >= 128 else 1),
             "clocks": clk.summary(), "impl": "ours",
         }
         print(json.dumps(line), flush=True)

@@ -433,9 +433,63 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
 
 // lb: lazy bound selected from the moduli (16: all < 2^60, 8: all < 2^61,
 // 4: up to 62 bits)
+int run_polymul_one(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
+                    const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
+                    int phases, cudaStream_t st);
+
+// Two-stream split of a large fused batch (n > 4096, full product): the
+// second half runs on an internal stream, so the HBM-bound column launches
+// of one half overlap the integer-bound row launch of the other (sweep:
+// +2.7 % on cfg3, scripts/stream_overlap.py).  Fork / join with events on
+// the caller's stream, so callers still see one ordered operation.
+#ifndef NTTB_SPLIT_STREAMS
+#define NTTB_SPLIT_STREAMS 2
+#endif
 int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
                 const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
                 int phases, cudaStream_t st) {
+  constexpr int K = NTTB_SPLIT_STREAMS;
+  const bool split = K > 1 && phases == 7 && log_n > COL_LOG_R && g_chunk_waves == 0 &&
+                     npolys >= 64 * K && !g_group;
+  if (!split)
+    return run_polymul_one(mode, lb, c, a, b, ws, tw, ls, log_n, npolys, phases, st);
+  struct Side {
+    cudaStream_t s[K];
+    cudaEvent_t fork, join[K];
+  };
+  static Side sides[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cuda_status("device");
+  Side &sd = sides[dev];
+  if (!sd.s[0]) {
+    if (cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_status("split streams");
+    for (int k = 0; k < K; ++k)
+      if (cudaStreamCreateWithFlags(&sd.s[k], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&sd.join[k], cudaEventDisableTiming) != cudaSuccess)
+        return cuda_status("split streams");
+  }
+  if (cudaEventRecord(sd.fork, st) != cudaSuccess) return cuda_status("split fork");
+  const long long n = 1LL << log_n;
+  long long off = 0;
+  for (int k = 0; k < K; ++k) {
+    const long long cnt = (npolys - off) / (K - k);
+    if (cudaStreamWaitEvent(sd.s[k], sd.fork) != cudaSuccess) return cuda_status("split wait");
+    LimbSet lk = ls;
+    lk.base = static_cast<int>((ls.base + off) % (ls.num > 0 ? ls.num : 1));
+    CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw, lk,
+                          log_n, cnt, phases, sd.s[k]));
+    if (cudaEventRecord(sd.join[k], sd.s[k]) != cudaSuccess ||
+        cudaStreamWaitEvent(st, sd.join[k]) != cudaSuccess)
+      return cuda_status("split join");
+    off += cnt;
+  }
+  return NTTMUL_OK;
+}
+
+int run_polymul_one(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
+                    const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
+                    int phases, cudaStream_t st) {
 #define NTTB_PM(M, LBV) run_polymul_m<M, LBV>(c, a, b, ws, tw, ls, log_n, npolys, phases, st)
   if (lb == 16) {
     switch (mode) {
