@@ -445,12 +445,15 @@ int run_polymul_one(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *w
 #ifndef NTTB_SPLIT_STREAMS
 #define NTTB_SPLIT_STREAMS 2
 #endif
+#ifndef NTTB_SPLIT_PARTS
+#define NTTB_SPLIT_PARTS NTTB_SPLIT_STREAMS  // parts, assigned round-robin to the streams
+#endif
 int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
                 const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
                 int phases, cudaStream_t st) {
-  constexpr int K = NTTB_SPLIT_STREAMS;
+  constexpr int K = NTTB_SPLIT_STREAMS, NP = NTTB_SPLIT_PARTS;
   const bool split = K > 1 && phases == 7 && log_n > COL_LOG_R && g_chunk_waves == 0 &&
-                     npolys >= 64 * K && !g_group;
+                     npolys >= 64 * NP && !g_group;
   if (!split)
     return run_polymul_one(mode, lb, c, a, b, ws, tw, ls, log_n, npolys, phases, st);
   struct Side {
@@ -471,19 +474,21 @@ int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
   }
   if (cudaEventRecord(sd.fork, st) != cudaSuccess) return cuda_status("split fork");
   const long long n = 1LL << log_n;
-  long long off = 0;
-  for (int k = 0; k < K; ++k) {
-    const long long cnt = (npolys - off) / (K - k);
+  for (int k = 0; k < K; ++k)
     if (cudaStreamWaitEvent(sd.s[k], sd.fork) != cudaSuccess) return cuda_status("split wait");
+  long long off = 0;
+  for (int p = 0; p < NP; ++p) {
+    const long long cnt = (npolys - off) / (NP - p);
     LimbSet lk = ls;
     lk.base = static_cast<int>((ls.base + off) % (ls.num > 0 ? ls.num : 1));
     CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw, lk,
-                          log_n, cnt, phases, sd.s[k]));
+                          log_n, cnt, phases, sd.s[p % K]));
+    off += cnt;
+  }
+  for (int k = 0; k < K; ++k)
     if (cudaEventRecord(sd.join[k], sd.s[k]) != cudaSuccess ||
         cudaStreamWaitEvent(st, sd.join[k]) != cudaSuccess)
       return cuda_status("split join");
-    off += cnt;
-  }
   return NTTMUL_OK;
 }
 
