@@ -58,6 +58,44 @@ __device__ __forceinline__ Limb get_limb(const LimbSet &S, long long poly,
   return S.single;
 }
 
+// L2 eviction-priority hints for the global streams of the pipeline:
+// inputs read for the last time are loaded evict-first, intermediates that
+// the next launch reads again (a', b' -> row kernel, c' -> inverse columns)
+// are stored evict-last, the final product evict-first.  NTTB_L2_HINTS=0
+// turns them into plain accesses.
+#ifndef NTTB_L2_HINTS
+#define NTTB_L2_HINTS 0  // measured +-0 % on the step, inverse columns slower (sweep_r33)
+#endif
+enum L2Hint { L2_NORMAL = 0, L2_FIRST = 1, L2_LAST = 2 };
+
+template <int H>
+__device__ __forceinline__ u64 l2_policy() {
+  u64 pol = 0;
+  if (H == L2_FIRST)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else if (H == L2_LAST)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+template <int H>
+__device__ __forceinline__ u64 ldg_hint(const u64 *p) {
+  if (!NTTB_L2_HINTS || H == L2_NORMAL) return *p;
+  u64 v;
+  asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(l2_policy<H>()));
+  return v;
+}
+
+template <int H>
+__device__ __forceinline__ void stg_hint(u64 *p, u64 v) {
+  if (!NTTB_L2_HINTS || H == L2_NORMAL) {
+    *p = v;
+    return;
+  }
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(l2_policy<H>())
+               : "memory");
+}
+
 // Drop a consumed scratch line from L2 without writing it back to HBM
 // (sm_80+ discard.global.L2): intermediates of the fused pipeline live and
 // die in L2.  `line` must be 128-byte aligned and fully consumed.
@@ -188,7 +226,7 @@ __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
 #pragma unroll
       for (int e = 0; e < (1 << R); ++e) {
         const int o = o0 + (e << LK);
-        x[0][e] = FROM_GLOBAL ? g[o] : s[G::idx(o)];
+        x[0][e] = FROM_GLOBAL ? ldg_hint<L2_FIRST>(g + o) : s[G::idx(o)];
       }
 #if NTTB_TW_PREFETCH
       fwd_radix_pf<LB, R, R, 1, S0 & 1>(x, twb, M);
@@ -231,7 +269,7 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
 #endif
       inv_stage0<LB, R, 1>(x, B0, tw, L, M, fin);
 #pragma unroll
-      for (int e = 0; e < (1 << R); ++e) gout[o0 + (e << LK)] = x[0][e];
+      for (int e = 0; e < (1 << R); ++e) stg_hint<L2_LAST>(gout + o0 + (e << LK), x[0][e]);
     } else {
 #if NTTB_TW_PREFETCH
       inv_radix_pf<LB, R, R, 0, 1>(x, twb, M);
@@ -303,7 +341,13 @@ __device__ __forceinline__ void head_inv_all(u64 *sm, u64 *gout, u64 rowbase,
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+#if NTTB_L2_HINTS
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem),
+               "l"(l2_policy<L2_FIRST>())
+               : "memory");
+#else
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -679,7 +723,7 @@ __global__ void __launch_bounds__(COL_THREADS, ColGeom<INV>::MINB) col_kernel(co
       x[0][e] = v.x;
       x[V - 1][e] = v.y;
     } else {
-      x[0][e] = src[o];
+      x[0][e] = ldg_hint<L2_FIRST>(src + o);
     }
   }
   if (!INV) {
@@ -700,7 +744,10 @@ __global__ void __launch_bounds__(COL_THREADS, ColGeom<INV>::MINB) col_kernel(co
     if (V == 2) {
       *reinterpret_cast<ulonglong2 *>(dst + o) = make_ulonglong2(x[0][e], x[V - 1][e]);
     } else {
-      dst[o] = x[0][e];
+      if (INV)
+        stg_hint<L2_FIRST>(dst + o, x[0][e]);  // the product: not read again here
+      else
+        stg_hint<L2_LAST>(dst + o, x[0][e]);   // a', b': the row kernel reads them next
     }
   }
 }
