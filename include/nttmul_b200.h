@@ -57,6 +57,10 @@ extern "C" {
  * 2^60: the forward transform then corrects only every other stage
  * ([0, 16q) range).  Setting it with a larger modulus gives wrong results. */
 #define NTTMUL_MODE_NARROW60 0x200
+/* OR-ed in (with NTTMUL_MODE_NARROW60) when EVERY modulus has at least 35
+ * bits: the fused product's middle then uses multiply-based partial
+ * reductions instead of conditional-subtraction chains. */
+#define NTTMUL_MODE_WIDE35 0x400
 
 /* largest supported transform: n = 2^17 (BASELINE cfg4) */
 #define NTTMUL_MAX_LOG_N 17

@@ -500,6 +500,7 @@ int run_polymul_one(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *w
     switch (mode) {
       case 0: return NTTB_PM(0, 16);
       case 1: return NTTB_PM(1, 16);
+      case MODE_FASTRED: return NTTB_PM(MODE_FASTRED, 16);
       default: return NTTB_PM(2, 16);
     }
   }
@@ -791,8 +792,12 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
   if (c == b && log_n > COL_LOG_R)
     return fail(NTTMUL_EINVAL, "c may not alias b");
   const int lb = (mode & NTTMUL_MODE_NARROW60) ? 16 : ((mode & NTTMUL_MODE_NARROW) ? 8 : 4);
-  mode &= ~(NTTMUL_MODE_NARROW | NTTMUL_MODE_NARROW60);
+  const bool wide35 = (mode & NTTMUL_MODE_WIDE35) != 0;
+  mode &= ~(NTTMUL_MODE_NARROW | NTTMUL_MODE_NARROW60 | NTTMUL_MODE_WIDE35);
   if (mode < 0 || mode > 2) return fail(NTTMUL_EINVAL, "unknown reduction mode %d", mode);
+  // internal mode 3 = proposed-shape constants + multiply-based reductions
+  // in the lazy middle (all moduli in [2^34, 2^60))
+  if (mode == NTTMUL_RED_ONE_SUB && lb == 16 && wide35) mode = MODE_FASTRED;
   LimbSet ls;
   ls.table = limbs;
   ls.num = num_limbs;

@@ -22,6 +22,10 @@ namespace nttb {
 typedef uint64_t u64;
 typedef nttmul_limb_t Limb;
 
+// internal reduction mode: NTTMUL_RED_ONE_SUB constants, and every modulus
+// in [2^34, 2^60) so the lazy middle can use multiply-based reductions
+constexpr int MODE_FASTRED = 3;
+
 // x >= m ? x - m : x.
 // NTTB_CSUB_CARRY: the borrow of the 64-bit subtraction (a PTX carry chain)
 // selects the result - IADD3 + IADD3.X (carry out) + 2 predicated moves, but
@@ -59,7 +63,7 @@ __device__ __forceinline__ u64 mulred(u64 a, u64 b, const Limb &L) {
   const u64 quot = __umul64hi(c, L.mu_sh) >> L.s_hi;
   u64 r = lo - quot * L.q;  // exact: true remainder + (<=2) q < 2^64
   r = csub(r, L.q);
-  if (MODE == NTTMUL_RED_TWO_SUB) r = csub(r, L.q);
+  if (MODE == NTTMUL_RED_TWO_SUB) r = csub(r, L.q);  // MODE_FASTRED: one subtraction
   return r;
 }
 
@@ -301,24 +305,67 @@ __device__ __forceinline__ u64 to2q_fwd16(u64 x, const Mod &M) {
   return csub(csub(csub(x, M.q8), M.q4), M.q2);
 }
 
+
+
+// Multiply-based partial reduction of any x < 2^64 to [0, 2q) for moduli of
+// 35..62 bits: k = floor(hi32(x) r / 2^(32+s)) with r = floor(2^(64+s)/q) - 1
+// < 2^32 (s = bits(q) - 33) undershoots floor(x/q) by at most 1 (the dropped
+// low word contributes < 2^(33-bits) and r's truncation < 2^-26), so
+// x - k q lies in [0, 2q).  One IMAD.HI + one IMAD.WIDE + IMAD + a 64-bit
+// subtract, instead of a chain of conditional subtractions.
+struct FastRed {
+  uint32_t r;
+  uint32_t s;
+  bool ok;  // false: modulus too small, use the csub chain
+};
+
+__device__ __forceinline__ FastRed make_fastred(u64 q) {
+  FastRed f;
+  const int m = 64 - __clzll(static_cast<long long>(q));
+  f.ok = m >= 35 && m <= 62;
+  f.s = f.ok ? static_cast<uint32_t>(m - 33) : 0;
+  const double rd = ldexp(1.0, 64 + static_cast<int>(f.s)) / static_cast<double>(q);
+  f.r = f.ok ? static_cast<uint32_t>(rd) - 1 : 0;  // rd < 2^32; -1 absorbs rounding
+  return f;
+}
+
+__device__ __forceinline__ u64 reduce2q(u64 x, const FastRed &F, u64 q) {
+  uint32_t k;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(k) : "r"(hi32(x)), "r"(F.r));
+  k >>= F.s;
+  return x - (mulw(k, lo32(q)) + (static_cast<u64>(k * hi32(q)) << 32));
+}
+
+// forward-range value (LB = 16) -> [0, 2q)
+template <bool FAST>
+__device__ __forceinline__ u64 to2q_any(u64 x, const Mod &M, const FastRed &F) {
+  return FAST ? reduce2q(x, F, M.q) : to2q_fwd16(x, M);
+}
+
 // Lazy Karatsuba-fused middle pair for the LB = 16 path (all q < 2^60,
 // proposed-shape Barrett constants): inputs in [0, 2q), outputs c0, c1 in
 // [0, 4q) (the inverse lazy range, so the inverse stages take them as is).
 // Same algebra as fused_pair / reference _kernels.pyx:142-173; canonical
 // results after the inverse transform are identical.
+template <bool FAST>
 __device__ __forceinline__ void fused_pair_lazy(u64 a0, u64 a1, u64 b0, u64 b1, u64 w, u64 wp,
                                                 bool odd, const Limb &L, const Mod &M,
-                                                u64 &c0, u64 &c1) {
+                                                const FastRed &F, u64 &c0, u64 &c1) {
   const u64 u = mulred_lazy(a0, b0, L, M);         // [0, 5q)
   const u64 v = mulred_lazy(a1, b1, L, M);         // [0, 5q)
   const u64 s1 = csub(a0 + a1, M.q2);              // [0, 2q)
   const u64 s2 = csub(b0 + b1, M.q2);
   const u64 ww = mulred_lazy(s1, s2, L, M);        // [0, 5q)
   const u64 y = ww + M.q8 + M.q2 - u - v;          // (0, 15q)
-  c1 = csub(csub(y, M.q8), M.q4);                  // [0, 4q)
   const u64 z = shoup4(v, w, wp, M);               // [0, 4q)
   const u64 x = odd ? u + M.q4 - z : u + z;        // [0, 9q)
-  c0 = csub(csub(x, M.q8), M.q4);                  // [0, 4q)
+  if (FAST) {  // -> [0, 2q)
+    c1 = reduce2q(y, F, M.q);
+    c0 = reduce2q(x, F, M.q);
+  } else {  // -> [0, 4q)
+    c1 = csub(csub(y, M.q8), M.q4);
+    c0 = csub(csub(x, M.q8), M.q4);
+  }
 }
 
 }  // namespace nttb

@@ -147,6 +147,9 @@ enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 #ifndef NTTB_LAZY_MID
 #define NTTB_LAZY_MID 1
 #endif
+#ifndef NTTB_FAST_RED
+#define NTTB_FAST_RED 1
+#endif
 // issue a unit's twiddle loads before its data loads (hides their L2
 // latency; measured -2.7 % row-kernel time, sweep_r18)
 #ifndef NTTB_TW_PREFETCH
@@ -388,7 +391,13 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   constexpr int E = G::E;
   constexpr int LE = G::HEAD == 0 ? 0 : LOG_R - G::HEAD;  // = LOG_E
   // lazy Barrett middle (proposed/dhem constants, all moduli < 2^60)
-  constexpr bool LAZY_MID = NTTB_LAZY_MID && MODE == NTTMUL_RED_ONE_SUB && LB == 16;
+  constexpr bool LAZY_MID =
+      NTTB_LAZY_MID && (MODE == NTTMUL_RED_ONE_SUB || MODE == MODE_FASTRED) && LB == 16;
+  // multiply-based partial reductions around the middle (moduli of 35+ bits)
+  constexpr bool FAST = LAZY_MID && MODE == MODE_FASTRED && NTTB_FAST_RED;
+  FastRed F;
+  F.ok = false;
+  if constexpr (FAST && MID) F = make_fastred(M.q);
   const int o0 = threadIdx.x * E;
   const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
 #if NTTB_TW_PREFETCH
@@ -408,7 +417,8 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
 #endif
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      sm[G::idx(o0 + e)] = LAZY_MID ? to2q_fwd16(xa[0][e], M) : canon_fwd<LB>(xa[0][e], M);
+      sm[G::idx(o0 + e)] =
+          LAZY_MID ? to2q_any<FAST>(xa[0][e], M, F) : canon_fwd<LB>(xa[0][e], M);
 #pragma unroll
     for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + G::idx(o0 + e)];
 #if NTTB_TW_PREFETCH
@@ -427,9 +437,10 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
       for (int h = 0; h < 2; ++h) {
         const int i0 = 2 * (p + h);
         if constexpr (LAZY_MID)
-          fused_pair_lazy(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
-                          to2q_fwd16(xa[0][i0], M), to2q_fwd16(xa[0][i0 + 1], M), w.x, w.y,
-                          h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
+          fused_pair_lazy<FAST>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
+                                to2q_any<FAST>(xa[0][i0], M, F),
+                                to2q_any<FAST>(xa[0][i0 + 1], M, F), w.x, w.y, h != 0, L, M, F,
+                                xa[0][i0], xa[0][i0 + 1]);
         else
           fused_pair<MODE>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
                            canon_fwd<LB>(xa[0][i0], M), canon_fwd<LB>(xa[0][i0 + 1], M),

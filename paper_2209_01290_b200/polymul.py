@@ -181,11 +181,15 @@ MODE_NARROW = 0x100    # NTTMUL_MODE_NARROW: every modulus < 2^61 ([0, 8q) lazy 
 MODE_NARROW60 = 0x200  # NTTMUL_MODE_NARROW60: every modulus < 2^60 ([0, 16q) forward)
 
 
+MODE_WIDE35 = 0x400    # NTTMUL_MODE_WIDE35: every modulus >= 2^34 (multiply-based reductions)
+
+
 def mode_flags(mode: int, primes) -> int:
     """Reduction mode plus the lazy-bound flags the moduli allow."""
     top = max(primes)
     if top < (1 << 60):
-        return mode | MODE_NARROW | MODE_NARROW60
+        wide = MODE_WIDE35 if min(primes).bit_length() >= 35 else 0
+        return mode | MODE_NARROW | MODE_NARROW60 | wide
     return mode | (MODE_NARROW if top < (1 << 61) else 0)
 
 

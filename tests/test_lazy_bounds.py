@@ -97,3 +97,40 @@ def test_mulred_lazy_range(q, variant):
         b = rng.choice(edge + [rng.randrange(2 * q)])
         r = mulred_lazy(a, b, q, mu_sh, s_in, s_hi)
         assert r % q == a * b % q and r < 5 * q
+
+
+def make_fastred(q):
+    """modarith.cuh make_fastred: (r, s, ok) with r = floor(2^(64+s) / q) - 1
+    computed through a double division like the device code."""
+    import math
+
+    m = q.bit_length()
+    if not 35 <= m <= 62:
+        return 0, 0, False
+    s = m - 33
+    rd = math.ldexp(1.0, 64 + s) / float(q)
+    return int(rd) - 1, s, True
+
+
+def reduce2q(x, q, r, s):
+    k = ((x >> 32) * r >> 32) >> s
+    return (x - k * q) & M64
+
+
+@pytest.mark.parametrize("q", [(1 << 34) + 1, (1 << 35) - 31, 998244353 * 64 + 1,
+                               576460752303816705, 1152921504606830593,
+                               1152921504606584833, (1 << 62) - 57])
+def test_reduce2q_range(q):
+    """Multiply-based partial reduction: x - k q in [0, 2q) for any x < 2^64
+    (the fused middle's inputs < 16q and outputs < 15q included)."""
+    r, s, ok = make_fastred(q)
+    if q.bit_length() < 35:
+        assert not ok
+        return
+    assert ok and r < (1 << 32)
+    rng = random.Random(q)
+    for _ in range(50000):
+        x = rng.choice([rng.randrange(1 << 64), rng.randrange(16 * q) if 16 * q < (1 << 64)
+                        else rng.randrange(1 << 64), M64, 0, q - 1, q, 2 * q - 1, 2 * q])
+        y = reduce2q(x, q, r, s)
+        assert y % q == x % q and y < 2 * q, (x, y)
