@@ -329,7 +329,9 @@ int nttmul_set_group(int enable);
  * every thread runs `iters` iterations of `chains` independent dependent
  * modmul chains.  kind 0 = Barrett data*data (mode from limb), 1 = Shoup
  * (fixed multiplicand), 2 = lazy forward CT butterfly, 3 = lazy inverse GS
- * butterfly (kinds 2/3 count one modmul per butterfly; need q < 2^61).  Writes an XOR sink to *sink_out so the work cannot
+ * butterfly (kinds 2/3 count one modmul per butterfly; need q < 2^61),
+ * 4 / 5 = the forward / inverse butterflies of the multiply-reduced LB = 32
+ * schedule (reduce-plain-plain / reduce-plain; need a 35..60-bit q).  Writes an XOR sink to *sink_out so the work cannot
  * be elided.  Returns the number of modmuls issued in *modmuls_out (host).
  */
 int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks,

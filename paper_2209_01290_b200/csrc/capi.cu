@@ -311,6 +311,10 @@ int g_chunk_waves = 0;  // row-kernel waves per pipeline chunk (0: no chunking; 
 #endif
 int g_group = NTTB_GROUP;
 
+#ifndef NTTB_LB32
+#define NTTB_LB32 1  // multiply-reduced lazy schedule for moduli of 35..59 bits
+#endif
+
 // Cooperative launch of group_fused_kernel.  Returns NTTMUL_OK, or -1 when
 // the batch is too small for the group scheme (the caller falls back to the
 // three-launch pipeline).
@@ -496,11 +500,11 @@ int run_polymul_one(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *w
                     const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
                     int phases, cudaStream_t st) {
 #define NTTB_PM(M, LBV) run_polymul_m<M, LBV>(c, a, b, ws, tw, ls, log_n, npolys, phases, st)
+  if (lb == 32) return NTTB_PM(2, 32);  // proposed-shape constants only (see caller)
   if (lb == 16) {
     switch (mode) {
       case 0: return NTTB_PM(0, 16);
       case 1: return NTTB_PM(1, 16);
-      case MODE_FASTRED: return NTTB_PM(MODE_FASTRED, 16);
       default: return NTTB_PM(2, 16);
     }
   }
@@ -795,9 +799,10 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
   const bool wide35 = (mode & NTTMUL_MODE_WIDE35) != 0;
   mode &= ~(NTTMUL_MODE_NARROW | NTTMUL_MODE_NARROW60 | NTTMUL_MODE_WIDE35);
   if (mode < 0 || mode > 2) return fail(NTTMUL_EINVAL, "unknown reduction mode %d", mode);
-  // internal mode 3 = proposed-shape constants + multiply-based reductions
-  // in the lazy middle (all moduli in [2^34, 2^60))
-  if (mode == NTTMUL_RED_ONE_SUB && lb == 16 && wide35) mode = MODE_FASTRED;
+  // lazy bound "32": the [0, 16q) ranges with multiply-based reductions
+  // (every modulus in [2^34, 2^60)), for the proposed-shape constants
+  int lbx = lb;
+  if (mode == NTTMUL_RED_ONE_SUB && lb == 16 && wide35) lbx = NTTB_LB32 ? 32 : 16;
   LimbSet ls;
   ls.table = limbs;
   ls.num = num_limbs;
@@ -806,7 +811,7 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
   const long long stride = 1LL << log_n;
   TwSet tw{reinterpret_cast<const ulonglong2 *>(fwd_pairs),
            reinterpret_cast<const ulonglong2 *>(inv_pairs), stride};
-  return run_polymul(mode, lb, c, a, b, workspace, tw, ls, log_n,
+  return run_polymul(mode, lbx, c, a, b, workspace, tw, ls, log_n,
                      batch * num_limbs, phases, S(stream));
 }
 
@@ -1039,6 +1044,17 @@ int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int
       modmul_roof_kernel<2, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
     else
       modmul_roof_kernel<3, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
+    if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2);
+    return cuda_status("modmul_roof_kernel");
+  } else if (kind == 4 || kind == 5) {
+    const int bits = 64 - __builtin_clzll(L.q);
+    if (bits < 35 || bits > 60) return fail(NTTMUL_EINVAL, "LB=32 roof needs a 35..60-bit q");
+    if (kind == 4)
+      modmul_roof_kernel<4, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
+    else
+      modmul_roof_kernel<5, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
+    if (modmuls_out)
+      *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2) * (kind == 4 ? 3 : 2);
     if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2);
     return cuda_status("modmul_roof_kernel");
   } else {

@@ -22,9 +22,7 @@ namespace nttb {
 typedef uint64_t u64;
 typedef nttmul_limb_t Limb;
 
-// internal reduction mode: NTTMUL_RED_ONE_SUB constants, and every modulus
-// in [2^34, 2^60) so the lazy middle can use multiply-based reductions
-constexpr int MODE_FASTRED = 3;
+
 
 // x >= m ? x - m : x.
 // NTTB_CSUB_CARRY: the borrow of the 64-bit subtraction (a PTX carry chain)
@@ -63,7 +61,7 @@ __device__ __forceinline__ u64 mulred(u64 a, u64 b, const Limb &L) {
   const u64 quot = __umul64hi(c, L.mu_sh) >> L.s_hi;
   u64 r = lo - quot * L.q;  // exact: true remainder + (<=2) q < 2^64
   r = csub(r, L.q);
-  if (MODE == NTTMUL_RED_TWO_SUB) r = csub(r, L.q);  // MODE_FASTRED: one subtraction
+  if (MODE == NTTMUL_RED_TWO_SUB) r = csub(r, L.q);
   return r;
 }
 
@@ -109,6 +107,7 @@ __device__ __forceinline__ u64 pack(uint32_t lo, uint32_t hi) {
 struct Mod {
   u64 q, q2, q4, q8;
   uint32_t nql, nqh;  // halves of 2^64 - q
+  uint32_t fr, fs;    // LB = 32 only: multiply-based reduction constants (reduce2q)
 };
 
 __device__ __forceinline__ Mod make_mod(u64 q) {
@@ -120,7 +119,42 @@ __device__ __forceinline__ Mod make_mod(u64 q) {
   const u64 nq = 0 - q;
   m.nql = lo32(nq);
   m.nqh = hi32(nq);
+  m.fr = 0;
+  m.fs = 0;
   return m;
+}
+
+// Multiply-based partial reduction of any x < 2^64 to [0, 2q) for moduli of
+// 35..62 bits: k = floor(hi32(x) r / 2^(32+s)) with r = floor(2^(64+s)/q) - 1
+// < 2^32 (s = bits(q) - 33) undershoots floor(x/q) by at most 1 (the dropped
+// low word contributes < 2^(33-bits) and r's truncation < 2^-26), so
+// x - k q lies in [0, 2q).  One IMAD.HI + one IMAD.WIDE + IMAD + a 64-bit
+// subtract, instead of a chain of conditional subtractions.  The constants
+// come from a double division (rd < 2^32; the -1 absorbs its rounding).
+__device__ __forceinline__ Mod make_mod_fast(u64 q) {
+  Mod m = make_mod(q);
+  const int bits = 64 - __clzll(static_cast<long long>(q));
+  m.fs = static_cast<uint32_t>(bits - 33);
+  const double rd = ldexp(1.0, 64 + static_cast<int>(m.fs)) / static_cast<double>(q);
+  m.fr = static_cast<uint32_t>(rd) - 1;
+  return m;
+}
+
+// LB = 32: the LB = 16 lazy ranges for moduli of 35..60 bits, where the
+// fused middle's partial reductions are multiply-based (reduce2q); with
+// NTTB_LB32_STAGES the transform stages use them too (measured slower: the
+// IMAD.HI / IMAD.WIDE quotient lands on the already busier multiply pipe).
+// Other bounds use plain constants.
+template <int LB>
+__device__ __forceinline__ Mod mod_for(u64 q) {
+  return LB == 32 ? make_mod_fast(q) : make_mod(q);
+}
+
+__device__ __forceinline__ u64 reduce2q(u64 x, const Mod &M) {
+  uint32_t k;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(k) : "r"(hi32(x)), "r"(M.fr));
+  k >>= M.fs;
+  return x - (mulw(k, lo32(M.q)) + (static_cast<u64>(k * hi32(M.q)) << 32));
 }
 
 // floor(x * y / 2^64) - e, e in {0, 1}: the high word from three of the
@@ -201,9 +235,20 @@ __device__ __forceinline__ u64 mulred_lazy(u64 a, u64 b, const Limb &L, const Mo
 // LB = 16 (moduli < 2^60) alternates reducing (RED) and non-reducing stages:
 // a RED stage takes X < 16q to [0, 8q) and emits < 12q, the next stage
 // skips the correction and emits < 16q - half the forward corrections.
+#ifndef NTTB_LB32_STAGES
+#define NTTB_LB32_STAGES 0  // 1: multiply-reduced stage schedule (measured slower: row 0.574 vs 0.551 ms, sweep_r35)
+#endif
+
 template <int LB, bool RED = true>
 __device__ __forceinline__ void ct_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod &M) {
-  if (LB == 16) {
+  if (LB == 32 && NTTB_LB32_STAGES) {
+    // RED stages (every third): X (any) -> [0, 2q), outputs < 6q; the two
+    // non-reducing stages after it emit < 10q and < 14q
+    const u64 x = RED ? reduce2q(X, M) : X;
+    const u64 t = shoup4(Y, w, wp, M);
+    X = x + t;
+    Y = x - t + M.q4;
+  } else if (LB >= 16) {
     const u64 x = RED ? csub(X, M.q8) : X;
     const u64 t = shoup4(Y, w, wp, M);
     X = x + t;
@@ -222,9 +267,16 @@ __device__ __forceinline__ void ct_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod
 }
 
 // Merged GS inverse butterfly (reference _kernels.pyx:102-118, unscaled).
-template <int LB>
+template <int LB, bool RED = true>
 __device__ __forceinline__ void gs_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod &M) {
-  if (LB >= 8) {
+  if (LB == 32 && NTTB_LB32_STAGES) {
+    // alternating: a RED stage takes X, Y < 8q and emits < 4q (sum reduced to
+    // [0, 2q)); the non-reducing stage after it takes < 4q and emits < 8q
+    const u64 s = RED ? reduce2q(X + Y, M) : X + Y;
+    const u64 d = X - Y + (RED ? M.q8 : M.q4);
+    X = s;
+    Y = shoup4(d, w, wp, M);
+  } else if (LB >= 8) {
     const u64 s = csub(X + Y, M.q4);
     const u64 d = X - Y + M.q4;
     X = s;
@@ -240,7 +292,7 @@ __device__ __forceinline__ void gs_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod
 // forward-range value -> [0, q)
 template <int LB>
 __device__ __forceinline__ u64 canon_fwd(u64 x, const Mod &M) {
-  if (LB == 16) x = csub(x, M.q8);
+  if (LB >= 16) x = csub(x, M.q8);
   if (LB >= 8) x = csub(x, M.q4);
   return csub(csub(x, M.q2), M.q);
 }
@@ -265,7 +317,7 @@ template <int LB>
 __device__ __forceinline__ void gs_bfly_last_scaled(u64 &X, u64 &Y, const u64 (&sc)[4],
                                                     const Mod &M) {
   const u64 s = X + Y;
-  const u64 d = X - Y + (LB >= 8 ? M.q4 : M.q2);
+  const u64 d = X - Y + (LB == 32 ? M.q8 : (LB >= 8 ? M.q4 : M.q2));
   X = shoup(s, sc[0], sc[1], M);
   Y = shoup(d, sc[2], sc[3], M);
 }
@@ -307,39 +359,10 @@ __device__ __forceinline__ u64 to2q_fwd16(u64 x, const Mod &M) {
 
 
 
-// Multiply-based partial reduction of any x < 2^64 to [0, 2q) for moduli of
-// 35..62 bits: k = floor(hi32(x) r / 2^(32+s)) with r = floor(2^(64+s)/q) - 1
-// < 2^32 (s = bits(q) - 33) undershoots floor(x/q) by at most 1 (the dropped
-// low word contributes < 2^(33-bits) and r's truncation < 2^-26), so
-// x - k q lies in [0, 2q).  One IMAD.HI + one IMAD.WIDE + IMAD + a 64-bit
-// subtract, instead of a chain of conditional subtractions.
-struct FastRed {
-  uint32_t r;
-  uint32_t s;
-  bool ok;  // false: modulus too small, use the csub chain
-};
-
-__device__ __forceinline__ FastRed make_fastred(u64 q) {
-  FastRed f;
-  const int m = 64 - __clzll(static_cast<long long>(q));
-  f.ok = m >= 35 && m <= 62;
-  f.s = f.ok ? static_cast<uint32_t>(m - 33) : 0;
-  const double rd = ldexp(1.0, 64 + static_cast<int>(f.s)) / static_cast<double>(q);
-  f.r = f.ok ? static_cast<uint32_t>(rd) - 1 : 0;  // rd < 2^32; -1 absorbs rounding
-  return f;
-}
-
-__device__ __forceinline__ u64 reduce2q(u64 x, const FastRed &F, u64 q) {
-  uint32_t k;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(k) : "r"(hi32(x)), "r"(F.r));
-  k >>= F.s;
-  return x - (mulw(k, lo32(q)) + (static_cast<u64>(k * hi32(q)) << 32));
-}
-
-// forward-range value (LB = 16) -> [0, 2q)
-template <bool FAST>
-__device__ __forceinline__ u64 to2q_any(u64 x, const Mod &M, const FastRed &F) {
-  return FAST ? reduce2q(x, F, M.q) : to2q_fwd16(x, M);
+// forward-range value (LB >= 16) -> [0, 2q)
+template <int LB>
+__device__ __forceinline__ u64 to2q_any(u64 x, const Mod &M) {
+  return LB == 32 ? reduce2q(x, M) : to2q_fwd16(x, M);
 }
 
 // Lazy Karatsuba-fused middle pair for the LB = 16 path (all q < 2^60,
@@ -350,7 +373,7 @@ __device__ __forceinline__ u64 to2q_any(u64 x, const Mod &M, const FastRed &F) {
 template <bool FAST>
 __device__ __forceinline__ void fused_pair_lazy(u64 a0, u64 a1, u64 b0, u64 b1, u64 w, u64 wp,
                                                 bool odd, const Limb &L, const Mod &M,
-                                                const FastRed &F, u64 &c0, u64 &c1) {
+                                                u64 &c0, u64 &c1) {
   const u64 u = mulred_lazy(a0, b0, L, M);         // [0, 5q)
   const u64 v = mulred_lazy(a1, b1, L, M);         // [0, 5q)
   const u64 s1 = csub(a0 + a1, M.q2);              // [0, 2q)
@@ -360,8 +383,8 @@ __device__ __forceinline__ void fused_pair_lazy(u64 a0, u64 a1, u64 b0, u64 b1, 
   const u64 z = shoup4(v, w, wp, M);               // [0, 4q)
   const u64 x = odd ? u + M.q4 - z : u + z;        // [0, 9q)
   if (FAST) {  // -> [0, 2q)
-    c1 = reduce2q(y, F, M.q);
-    c0 = reduce2q(x, F, M.q);
+    c1 = reduce2q(y, M);
+    c0 = reduce2q(x, M);
   } else {  // -> [0, 4q)
     c1 = csub(csub(y, M.q8), M.q4);
     c0 = csub(csub(x, M.q8), M.q4);

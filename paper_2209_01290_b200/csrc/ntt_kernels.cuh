@@ -391,13 +391,9 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   constexpr int E = G::E;
   constexpr int LE = G::HEAD == 0 ? 0 : LOG_R - G::HEAD;  // = LOG_E
   // lazy Barrett middle (proposed/dhem constants, all moduli < 2^60)
-  constexpr bool LAZY_MID =
-      NTTB_LAZY_MID && (MODE == NTTMUL_RED_ONE_SUB || MODE == MODE_FASTRED) && LB == 16;
-  // multiply-based partial reductions around the middle (moduli of 35+ bits)
-  constexpr bool FAST = LAZY_MID && MODE == MODE_FASTRED && NTTB_FAST_RED;
-  FastRed F;
-  F.ok = false;
-  if constexpr (FAST && MID) F = make_fastred(M.q);
+  constexpr bool LAZY_MID = NTTB_LAZY_MID && MODE == NTTMUL_RED_ONE_SUB && LB >= 16;
+  // multiply-based partial reductions around the middle (LB = 32)
+  constexpr bool FAST = LAZY_MID && LB == 32;
   const int o0 = threadIdx.x * E;
   const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
 #if NTTB_TW_PREFETCH
@@ -418,7 +414,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
 #pragma unroll
     for (int e = 0; e < E; ++e)
       sm[G::idx(o0 + e)] =
-          LAZY_MID ? to2q_any<FAST>(xa[0][e], M, F) : canon_fwd<LB>(xa[0][e], M);
+          LAZY_MID ? to2q_any<LB>(xa[0][e], M) : canon_fwd<LB>(xa[0][e], M);
 #pragma unroll
     for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + G::idx(o0 + e)];
 #if NTTB_TW_PREFETCH
@@ -438,9 +434,8 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
         const int i0 = 2 * (p + h);
         if constexpr (LAZY_MID)
           fused_pair_lazy<FAST>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
-                                to2q_any<FAST>(xa[0][i0], M, F),
-                                to2q_any<FAST>(xa[0][i0 + 1], M, F), w.x, w.y, h != 0, L, M, F,
-                                xa[0][i0], xa[0][i0 + 1]);
+                                to2q_any<LB>(xa[0][i0], M), to2q_any<LB>(xa[0][i0 + 1], M), w.x,
+                                w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
         else
           fused_pair<MODE>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
                            canon_fwd<LB>(xa[0][i0], M), canon_fwd<LB>(xa[0][i0 + 1], M),
@@ -519,7 +514,7 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
   const int r = static_cast<int>(row & ((1LL << P.log_n1) - 1));
   int limb;
   const Limb &L = *limb_ptr(P.limbs, poly, limb);
-  const Mod M = make_mod(L.q);
+  const Mod M = mod_for<LB>(L.q);
   const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
   const u64 rowbase = (1ULL << P.log_n1) + r;  // (N1 + r): group index base
@@ -627,7 +622,7 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T, NTTB_ROW_MINB_FUSED)
     const int r = static_cast<int>(row & ((1LL << P.log_n1) - 1));
     int limb;
     const Limb &L = *limb_ptr(P.limbs, poly, limb);
-    const Mod M = make_mod(L.q);
+    const Mod M = mod_for<LB>(L.q);
     const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
     const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
     const u64 rowbase = (1ULL << P.log_n1) + r;
@@ -722,7 +717,7 @@ __global__ void __launch_bounds__(COL_THREADS, ColGeom<INV>::MINB) col_kernel(co
       (poly << (COL_LOG_R + LOG_N1)) + (rem & ((1 << COL_LOG_R) - 1));
   int limb;
   const Limb &L = *limb_ptr(P.limbs, poly, limb);
-  const Mod M = make_mod(L.q);
+  const Mod M = mod_for<LB>(L.q);
   const u64 *__restrict__ src = (which ? P.src1 : P.src0) + base;
   u64 *__restrict__ dst = (which ? P.dst1 : P.dst0) + base;
   u64 x[V][N1];
@@ -883,7 +878,7 @@ __global__ void __launch_bounds__(ColPipeGeom<LOG_N1>::TC)
     where(t, which, poly, col0);
     int limb;
     const Limb &L = *limb_ptr(P.limbs, poly, limb);
-    const Mod M = make_mod(L.q);
+    const Mod M = mod_for<LB>(L.q);
     u64 *buf = csm + s * G::TILE_WORDS;
     bulk::mbar_wait(bars + s, (it / S) & 1);
     u64 x[1][N1];
@@ -987,7 +982,7 @@ __device__ __noinline__ void group_phase1(const GroupParams &P, long long p, int
   constexpr long long N = static_cast<long long>(N1) * N2;
   int limb;
   const Limb &L = *limb_ptr(P.limbs, p, limb);
-  const Mod M = make_mod(L.q);
+  const Mod M = mod_for<LB>(L.q);
   const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
 #pragma unroll 1
   for (int j = threadIdx.x; j < 2 * SW; j += blockDim.x) {
@@ -1013,7 +1008,7 @@ __device__ __noinline__ void group_phase2(const GroupParams &P, long long p, int
   constexpr long long N = static_cast<long long>(N1) * N2;
   int limb;
   const Limb &L = *limb_ptr(P.limbs, p, limb);
-  const Mod M = make_mod(L.q);
+  const Mod M = mod_for<LB>(L.q);
   const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
   const u64 rowbase = static_cast<u64>(N1) + i;
@@ -1042,7 +1037,7 @@ __device__ __noinline__ void group_phase3(const GroupParams &P, long long p, int
   constexpr long long N = static_cast<long long>(N1) * N2;
   int limb;
   const Limb &L = *limb_ptr(P.limbs, p, limb);
-  const Mod M = make_mod(L.q);
+  const Mod M = mod_for<LB>(L.q);
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
 #pragma unroll 1
   for (int j = threadIdx.x; j < SW; j += blockDim.x) {
@@ -1140,7 +1135,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
   const long long poly = blockIdx.x;
   int limb;
   const Limb L = get_limb(P.limbs, poly, limb);
-  const Mod M = make_mod(L.q);
+  const Mod M = mod_for<LB>(L.q);
   const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
   const long long off = poly * n;
@@ -1156,7 +1151,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
         const int i = b / k, j = 2 * i * k + (b % k);
         const ulonglong2 w = ldtw(twf, m + i);
         for (int p = 0; p < np; ++p)
-          if (LB != 16 || (stage & 1) == 0)
+          if (LB < 16 || (stage & 1) == 0)
             ct_bfly<LB, true>(sm[p * n + j], sm[p * n + j + k], w.x, w.y, M);
           else
             ct_bfly<LB, false>(sm[p * n + j], sm[p * n + j + k], w.x, w.y, M);
@@ -1313,7 +1308,7 @@ __global__ void __launch_bounds__(256)
     modmul_roof_kernel(long long iters, u64 *sink, const Limb L, u64 w,
                        u64 wp) {
   u64 x[CHAINS];
-  const Mod M = make_mod(L.q);
+  const Mod M = (KIND >= 4 && L.q >= (1ULL << 34)) ? make_mod_fast(L.q) : make_mod(L.q);
   const u64 seed = (blockIdx.x * 256ULL + threadIdx.x) * 0x9E3779B97F4A7C15ULL;
 #pragma unroll
   for (int c = 0; c < CHAINS; ++c) x[c] = (seed + c * 0x632BE59BD9B4E019ULL) % L.q;
@@ -1324,6 +1319,19 @@ __global__ void __launch_bounds__(256)
     } else if (KIND == 3) {  // inverse butterflies, [0, 4q)
 #pragma unroll
       for (int c = 0; c < CHAINS / 2; ++c) gs_bfly<8>(x[c], x[c + CHAINS / 2], w, wp, M);
+    } else if (KIND == 4) {  // forward butterflies, LB = 32 pattern (reduce, plain, plain)
+#pragma unroll
+      for (int c = 0; c < CHAINS / 2; ++c) {
+        ct_bfly<32, true>(x[c], x[c + CHAINS / 2], w, wp, M);
+        ct_bfly<32, false>(x[c], x[c + CHAINS / 2], w, wp, M);
+        ct_bfly<32, false>(x[c], x[c + CHAINS / 2], w, wp, M);
+      }
+    } else if (KIND == 5) {  // inverse butterflies, LB = 32 pattern (reduce, plain)
+#pragma unroll
+      for (int c = 0; c < CHAINS / 2; ++c) {
+        gs_bfly<32, true>(x[c], x[c + CHAINS / 2], w, wp, M);
+        gs_bfly<32, false>(x[c], x[c + CHAINS / 2], w, wp, M);
+      }
     } else {
 #pragma unroll
       for (int c = 0; c < CHAINS; ++c) {

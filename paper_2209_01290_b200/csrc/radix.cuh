@@ -45,7 +45,7 @@ __device__ __forceinline__ void fwd_radix(u64 (&x)[NP][1 << R], u64 B0,
         const int i0 = gi * 2 * half + e;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          if (((PAR + t) & 1) == 0)
+          if ((LB == 32 && NTTB_LB32_STAGES) ? (t % 3 == 0) : (((PAR + t) & 1) == 0))
             ct_bfly<LB, true>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
           else
             ct_bfly<LB, false>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
@@ -70,7 +70,12 @@ __device__ __forceinline__ void inv_radix(u64 (&x)[NP][1 << R], u64 B0,
       for (int e = 0; e < half; ++e) {
         const int i0 = gi * 2 * half + e;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) gs_bfly<LB>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+        for (int p = 0; p < NP; ++p) {
+          if (((TSTART - 1 - t) & 1) == 0)  // each call starts with a reducing stage
+            gs_bfly<LB, true>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+          else
+            gs_bfly<LB, false>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+        }
       }
     }
   }
@@ -109,7 +114,7 @@ __device__ __forceinline__ void fwd_radix_pf(u64 (&x)[NP][1 << R], const TwBuf<0
         const int i0 = gi * 2 * half + e;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          if (((PAR + t) & 1) == 0)
+          if ((LB == 32 && NTTB_LB32_STAGES) ? (t % 3 == 0) : (((PAR + t) & 1) == 0))
             ct_bfly<LB, true>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
           else
             ct_bfly<LB, false>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
@@ -133,7 +138,12 @@ __device__ __forceinline__ void inv_radix_pf(u64 (&x)[NP][1 << R], const TwBuf<0
       for (int e = 0; e < half; ++e) {
         const int i0 = gi * 2 * half + e;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) gs_bfly<LB>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+        for (int p = 0; p < NP; ++p) {
+          if (((TSTART - 1 - t) & 1) == 0)
+            gs_bfly<LB, true>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+          else
+            gs_bfly<LB, false>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
+        }
       }
     }
   }
