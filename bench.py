@@ -377,8 +377,11 @@ def modmul_roof(nt, basis, stream):
     limb = basis.plans[0].limb()
     sink = torch.zeros(1, dtype=torch.uint64, device="cuda")
     best = {}
-    for kind, label in ((1, "shoup"), (0, "barrett_proposed"), (2, "ct_butterfly"),
-                        (3, "gs_butterfly")):
+    # the forms the default fused schedule runs (the LB = 32 stage forms,
+    # kinds 4/5, and the shift-shaped-modulus forms, kinds 6/7, belong to
+    # opt-in schedules: NTTB_LB32_STAGES / NTTB_PM_SHIFT)
+    kinds = [(1, "shoup"), (0, "barrett_proposed"), (2, "ct_butterfly"), (3, "gs_butterfly")]
+    for kind, label in kinds:
         cnt = ctypes.c_double()
         args = (ctypes.byref(limb), kind, 148 * 8, 256, 2000, sink.data_ptr(),
                 ctypes.byref(cnt), stream.cuda_stream)

@@ -61,6 +61,12 @@ extern "C" {
  * bits: the fused product's middle then uses multiply-based partial
  * reductions instead of conditional-subtraction chains. */
 #define NTTMUL_MODE_WIDE35 0x400
+/* OR-ed in (with NTTMUL_MODE_WIDE35) when EVERY modulus q is "shift-shaped":
+ * hi32(2^64 - q) = 2^32 - 2^s for some s, i.e. q lies in
+ * [2^(32+s) - 2^32, 2^(32+s)) (e.g. the 60-bit NTT primes 2^60 - delta,
+ * delta < 2^32, that RnsBasis.build returns).  Products by the high word of
+ * -q then become shifts.  Setting it for other moduli gives wrong results. */
+#define NTTMUL_MODE_PM 0x800
 
 /* largest supported transform: n = 2^17 (BASELINE cfg4) */
 #define NTTMUL_MAX_LOG_N 17
@@ -331,8 +337,10 @@ int nttmul_set_group(int enable);
  * (fixed multiplicand), 2 = lazy forward CT butterfly, 3 = lazy inverse GS
  * butterfly (kinds 2/3 count one modmul per butterfly; need q < 2^61),
  * 4 / 5 = the forward / inverse butterflies of the multiply-reduced LB = 32
- * schedule (reduce-plain-plain / reduce-plain; need a 35..60-bit q).  Writes an XOR sink to *sink_out so the work cannot
- * be elided.  Returns the number of modmuls issued in *modmuls_out (host).
+ * schedule (reduce-plain-plain / reduce-plain; need a 35..60-bit q),
+ * 6 / 7 = the forward / inverse butterflies for shift-shaped moduli
+ * (NTTMUL_MODE_PM; reduce-plain).  Writes an XOR sink to *sink_out so the
+ * work cannot be elided.  Returns the number of modmuls issued in *modmuls_out (host).
  */
 int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks,
                        int threads, int64_t iters, uint64_t *sink_out,

@@ -8,6 +8,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "nttmul_b200.h"
@@ -93,7 +94,13 @@ int smem_optin(K kernel, size_t bytes) {
 template <int LOG_R, int FWD, bool MID, int INV, int MODE, int LB>
 int launch_row_t(const RowParams &P, long long rows, cudaStream_t st) {
   constexpr int NP = MID ? 2 : 1;
-  const size_t smem = NP * RowGeom<LOG_R>::PADN * sizeof(u64);
+  // NTTB_ROW_EXTRA_SMEM (bytes, experiments only): pad the dynamic shared
+  // memory to force fewer resident CTAs per SM
+  static const size_t extra = [] {
+    const char *e = std::getenv("NTTB_ROW_EXTRA_SMEM");
+    return e ? static_cast<size_t>(std::atol(e)) : size_t(0);
+  }();
+  const size_t smem = NP * RowGeom<LOG_R>::PADN * sizeof(u64) + extra;
   auto k = row_kernel<LOG_R, FWD, MID, INV, MODE, LB>;
   CHECK(smem_optin(k, smem));
   static long long slots = 0;  // resident CTAs per device for this instantiation
@@ -107,6 +114,9 @@ int launch_row_t(const RowParams &P, long long rows, cudaStream_t st) {
       nb = 1;
     }
     slots = static_cast<long long>(nb) * sms;
+    if (std::getenv("NTTB_DEBUG_OCC"))
+      std::fprintf(stderr, "row_kernel<%d,%d,%d,%d,%d,%d>: %d CTAs/SM, smem %zu\n", LOG_R, FWD,
+                   int(MID), INV, MODE, LB, nb, smem);
   }
   RowParams Q = P;
   Q.nrows = rows;
@@ -311,6 +321,12 @@ int g_chunk_waves = 0;  // row-kernel waves per pipeline chunk (0: no chunking; 
 #endif
 int g_group = NTTB_GROUP;
 
+#ifndef NTTB_PM_SHIFT
+// shift-shaped moduli (NTTMUL_MODE_PM): lazy bound "33".  Measured slower
+// (row kernel 0.568 vs 0.550 ms, pm_r36): ptxas moves the shift's subtract
+// onto the multiply pipe as IMAD.IADD, so the IMAD it replaces comes back.
+#define NTTB_PM_SHIFT 0
+#endif
 #ifndef NTTB_LB32
 #define NTTB_LB32 1  // multiply-reduced lazy schedule for moduli of 35..59 bits
 #endif
@@ -500,7 +516,8 @@ int run_polymul_one(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *w
                     const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
                     int phases, cudaStream_t st) {
 #define NTTB_PM(M, LBV) run_polymul_m<M, LBV>(c, a, b, ws, tw, ls, log_n, npolys, phases, st)
-  if (lb == 32) return NTTB_PM(2, 32);  // proposed-shape constants only (see caller)
+  if (lb == 33) return NTTB_PM(2, 33);  // proposed-shape constants only (see caller)
+  if (lb == 32) return NTTB_PM(2, 32);
   if (lb == 16) {
     switch (mode) {
       case 0: return NTTB_PM(0, 16);
@@ -797,12 +814,15 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
     return fail(NTTMUL_EINVAL, "c may not alias b");
   const int lb = (mode & NTTMUL_MODE_NARROW60) ? 16 : ((mode & NTTMUL_MODE_NARROW) ? 8 : 4);
   const bool wide35 = (mode & NTTMUL_MODE_WIDE35) != 0;
-  mode &= ~(NTTMUL_MODE_NARROW | NTTMUL_MODE_NARROW60 | NTTMUL_MODE_WIDE35);
+  const bool pm = (mode & NTTMUL_MODE_PM) != 0;
+  mode &= ~(NTTMUL_MODE_NARROW | NTTMUL_MODE_NARROW60 | NTTMUL_MODE_WIDE35 | NTTMUL_MODE_PM);
   if (mode < 0 || mode > 2) return fail(NTTMUL_EINVAL, "unknown reduction mode %d", mode);
   // lazy bound "32": the [0, 16q) ranges with multiply-based reductions
   // (every modulus in [2^34, 2^60)), for the proposed-shape constants
   int lbx = lb;
   if (mode == NTTMUL_RED_ONE_SUB && lb == 16 && wide35) lbx = NTTB_LB32 ? 32 : 16;
+  // "33": the same schedule with shift-shaped moduli (NTTMUL_MODE_PM)
+  if (lbx == 32 && pm && NTTB_PM_SHIFT) lbx = 33;
   LimbSet ls;
   ls.table = limbs;
   ls.num = num_limbs;
@@ -1055,7 +1075,17 @@ int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int
       modmul_roof_kernel<5, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
     if (modmuls_out)
       *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2) * (kind == 4 ? 3 : 2);
-    if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2);
+    return cuda_status("modmul_roof_kernel");
+  } else if (kind == 6 || kind == 7) {
+    const int bits = 64 - __builtin_clzll(L.q);
+    const uint32_t nqh = static_cast<uint32_t>((0 - L.q) >> 32), d = 0u - nqh;
+    if (bits < 35 || bits > 60 || d == 0 || (d & (d - 1)) != 0)
+      return fail(NTTMUL_EINVAL, "shift-shaped roof needs a 35..60-bit q with hi32(-q) = 2^32 - 2^s");
+    if (kind == 6)
+      modmul_roof_kernel<6, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
+    else
+      modmul_roof_kernel<7, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
+    if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2) * 2;
     return cuda_status("modmul_roof_kernel");
   } else {
     switch (L.mode) {

@@ -393,7 +393,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   // lazy Barrett middle (proposed/dhem constants, all moduli < 2^60)
   constexpr bool LAZY_MID = NTTB_LAZY_MID && MODE == NTTMUL_RED_ONE_SUB && LB >= 16;
   // multiply-based partial reductions around the middle (LB = 32)
-  constexpr bool FAST = LAZY_MID && LB == 32;
+  constexpr bool FAST = LAZY_MID && LB >= 32;
   const int o0 = threadIdx.x * E;
   const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
 #if NTTB_TW_PREFETCH
@@ -433,7 +433,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
       for (int h = 0; h < 2; ++h) {
         const int i0 = 2 * (p + h);
         if constexpr (LAZY_MID)
-          fused_pair_lazy<FAST>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
+          fused_pair_lazy<FAST, lb_pm<LB>()>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
                                 to2q_any<LB>(xa[0][i0], M), to2q_any<LB>(xa[0][i0 + 1], M), w.x,
                                 w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
         else
@@ -535,11 +535,13 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
     row_prefetch<LOG_R>(sm + G::PADN, P.in1 + off);
     cp_async_commit();
     head_fwd<LB, LOG_R, 0, G::R(0), 1, true>(sm, P.in0 + off, nullptr, rowbase, twf, M);
+    NTTB_STAMP(5);
     cp_async_wait<0>();
     __syncthreads();
     NTTB_STAMP(1);
     head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sm + G::PADN, nullptr, nullptr, rowbase, twf, M);
     __syncthreads();
+    NTTB_STAMP(6);
     head_fwd_all<LB, LOG_R, NP, 1>(sm, nullptr, nullptr, rowbase, twf, M);
     if (P.discard_in) {
       constexpr int LINES = G::N2 * 8 / 128;
@@ -572,6 +574,10 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
     head_inv_all<LB, LOG_R, G::NPASS - 1>(sm, P.out + off, rowbase, twi, L, M,
                                           P.log_n1 == 0 ? P.fin : FIN_LAZY);
     NTTB_STAMP(4);
+#ifdef NTTB_PHASE_TIMING
+    __syncthreads();  // the CTA's last warp
+    NTTB_STAMP(7);
+#endif
   } else {
 #pragma unroll 4
     for (int i = threadIdx.x; i < G::N2; i += G::T) P.out[off + i] = sm[G::idx(i)];
@@ -665,11 +671,14 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T, NTTB_ROW_MINB_FUSED)
 #ifndef NTTB_COL_VEC
 #define NTTB_COL_VEC 1
 #endif
+#ifndef NTTB_COL_SMEM_TW
+#define NTTB_COL_SMEM_TW 1
+#endif
 #ifndef NTTB_COL_MINB
 #define NTTB_COL_MINB 2
 #endif
 #ifndef NTTB_COL_MINB_INV
-#define NTTB_COL_MINB_INV 4
+#define NTTB_COL_MINB_INV 3
 #endif
 constexpr int COL_LOG_R = NTTB_COL_LOG_R;  // row length used for n > 2^COL_LOG_R
 constexpr int COL_THREADS = 256;
@@ -720,6 +729,18 @@ __global__ void __launch_bounds__(COL_THREADS, ColGeom<INV>::MINB) col_kernel(co
   const Mod M = mod_for<LB>(L.q);
   const u64 *__restrict__ src = (which ? P.src1 : P.src0) + base;
   u64 *__restrict__ dst = (which ? P.dst1 : P.dst0) + base;
+#if NTTB_COL_SMEM_TW
+  // The N1 - 1 column twiddles are the same for the whole CTA (its 256
+  // columns lie in one polynomial): stage them in shared memory so the
+  // butterflies read them just in time (LDS broadcast) instead of the
+  // compiler hoisting 2 x (N1 - 1) global loads into registers.
+  __shared__ ulonglong2 stw[N1];
+  {
+    const ulonglong2 *tg = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
+    if (threadIdx.x < N1) stw[threadIdx.x] = tg[threadIdx.x];
+    __syncthreads();
+  }
+#endif
   u64 x[V][N1];
 #pragma unroll
   for (int e = 0; e < N1; ++e) {
@@ -733,9 +754,17 @@ __global__ void __launch_bounds__(COL_THREADS, ColGeom<INV>::MINB) col_kernel(co
     }
   }
   if (!INV) {
+#if NTTB_COL_SMEM_TW
+    fwd_radix<LB, LOG_N1, LOG_N1, V>(x, 1, stw, M);
+#else
     fwd_radix<LB, LOG_N1, LOG_N1, V>(x, 1, P.tw.fwd + limb * P.tw.stride, M);
+#endif
   } else {
+#if NTTB_COL_SMEM_TW
+    const ulonglong2 *twi = stw;
+#else
     const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
+#endif
     inv_radix<LB, LOG_N1, LOG_N1, 1, V>(x, 1, twi, M);
     inv_stage0<LB, LOG_N1, V>(x, 1, twi, L, M, P.fin);
   }
@@ -1325,6 +1354,18 @@ __global__ void __launch_bounds__(256)
         ct_bfly<32, true>(x[c], x[c + CHAINS / 2], w, wp, M);
         ct_bfly<32, false>(x[c], x[c + CHAINS / 2], w, wp, M);
         ct_bfly<32, false>(x[c], x[c + CHAINS / 2], w, wp, M);
+      }
+    } else if (KIND == 6) {  // forward butterflies, shift-shaped moduli (LB = 33: reduce, plain)
+#pragma unroll
+      for (int c = 0; c < CHAINS / 2; ++c) {
+        ct_bfly<33, true>(x[c], x[c + CHAINS / 2], w, wp, M);
+        ct_bfly<33, false>(x[c], x[c + CHAINS / 2], w, wp, M);
+      }
+    } else if (KIND == 7) {  // inverse butterflies, shift-shaped moduli
+#pragma unroll
+      for (int c = 0; c < CHAINS / 2; ++c) {
+        gs_bfly<33, true>(x[c], x[c + CHAINS / 2], w, wp, M);
+        gs_bfly<33, false>(x[c], x[c + CHAINS / 2], w, wp, M);
       }
     } else if (KIND == 5) {  // inverse butterflies, LB = 32 pattern (reduce, plain)
 #pragma unroll

@@ -182,6 +182,13 @@ MODE_NARROW60 = 0x200  # NTTMUL_MODE_NARROW60: every modulus < 2^60 ([0, 16q) fo
 
 
 MODE_WIDE35 = 0x400    # NTTMUL_MODE_WIDE35: every modulus >= 2^34 (multiply-based reductions)
+MODE_PM = 0x800        # NTTMUL_MODE_PM: every hi32(2^64 - q) = 2^32 - 2^s (shift-shaped)
+
+
+def shift_shaped(q: int) -> bool:
+    """hi32(2^64 - q) == 2^32 - 2^s for some s (nttmul_b200.h NTTMUL_MODE_PM)."""
+    d = (1 << 32) - (((1 << 64) - q) >> 32)
+    return 0 < d < (1 << 32) and d & (d - 1) == 0
 
 
 def mode_flags(mode: int, primes) -> int:
@@ -189,6 +196,8 @@ def mode_flags(mode: int, primes) -> int:
     top = max(primes)
     if top < (1 << 60):
         wide = MODE_WIDE35 if min(primes).bit_length() >= 35 else 0
+        if wide and all(shift_shaped(q) for q in primes):
+            wide |= MODE_PM
         return mode | MODE_NARROW | MODE_NARROW60 | wide
     return mode | (MODE_NARROW if top < (1 << 61) else 0)
 

@@ -17,10 +17,14 @@ rows = min(B * L * 16, 1 << 16)
 buf = (ctypes.c_ulonglong * (8 * rows))()
 assert lib.nttmul_debug_phases(buf, rows) == 0
 t = np.frombuffer(buf, dtype=np.uint64).reshape(rows, 8).astype(np.int64)
-d = np.diff(t[:, :5], axis=1)
-names = ["pass0 (global load + 3 stages, a,b)", "head passes 1-2 (a,b)", "tail (fwd+middle+inv)",
-         "inverse head passes + store"]
+order = [0, 5, 1, 6, 2, 3, 4]
+names = ["a pass0 (global load + 3 stages)", "wait b (cp.async) + barrier", "b pass0 (smem)",
+         "passes 1-2 (a, b)", "tail (fwd + middle + inv)", "inverse passes + store"]
+d = np.diff(t[:, order], axis=1)
 tot = d.sum(1).mean()
 for i, n in enumerate(names):
     print(f"{n:40s} {d[:, i].mean():9.0f} cycles  {d[:, i].mean() / tot * 100:5.1f}%")
-print(f"{'total per CTA':40s} {tot:9.0f} cycles")
+print(f"{'total (warp 0)':40s} {tot:9.0f} cycles")
+print(f"{'CTA lifetime (start -> last warp done)':40s} {(t[:, 7] - t[:, 0]).mean():9.0f} cycles")
+sm_start = t[:, 0]
+print("rows", rows, "span of all CTAs (cycles, per-SM clocks differ)", int(t[:, 7].max() - t[:, 0].min()))
