@@ -53,17 +53,57 @@ def parse():
 # clocks sampled during the timed region (nvidia-smi, B200_PROFILING.md)
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled while the timed region runs:
+    NVML every ~2 ms (nvidia_ml_py; fast enough for a short region), else
+    nvidia-smi every 100 ms.  Rows: [sm_mhz, max_mhz, -, hw_slowdown,
+    hw_thermal, sw_thermal, sw_power_cap] ("Active"/"Not Active")."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits: HwSlowdown, HwThermalSlowdown, SwThermalSlowdown, SwPowerCap
+    NVML_BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, index: int):
         self.index = index
         self.rows: list[list[str]] = []
+        self.source = "nvidia-smi"
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_handle(self):
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            try:
+                uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(
+                    uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:  # noqa: BLE001 - older torch / MIG: fall back to the index
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            return pynvml, h
+        except Exception:  # noqa: BLE001 - NVML missing: nvidia-smi path
+            return None, None
+
     def _run(self):
+        nv, h = self._nv, self._h
+        if nv is not None:
+            self.source = "nvml"
+            try:
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                while not self._stop.is_set():
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    try:
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except AttributeError:
+                        rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    self.rows.append([str(sm), str(mx), hex(rs)] +
+                                     ["Active" if rs & b else "Not Active" for b in self.NVML_BITS])
+                    self._stop.wait(0.002)
+                return
+            except Exception:  # noqa: BLE001 - fall through to nvidia-smi
+                self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -77,11 +117,18 @@ class ClockSampler:
             self._stop.wait(0.1)
 
     def __enter__(self):
+        self._nv, self._h = self._nvml_handle()  # NVML init outside the region
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *exc):
+        # a very short timed region can end before the thread's first
+        # sample: give it up to 0.2 s to record one (clocks have not
+        # dropped yet right after the region)
+        t0 = time.perf_counter()
+        while not self.rows and self._t and self._t.is_alive() and time.perf_counter() - t0 < 0.2:
+            time.sleep(0.001)
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
@@ -96,7 +143,7 @@ class ClockSampler:
         reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7])
                           if v.lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
 # ---------------------------------------------------------------------------
@@ -464,10 +511,43 @@ def crt_rates(nt, basis, batch):
 
 
 def ntt_latency_us(nt, plan):
-    """Standalone ntt_ct latency, one limb (N=2^16), device-resident."""
+    """Standalone ntt_ct latency, one limb (N=2^16), device-resident: the
+    device time per transform from a CUDA graph of 20 back-to-back C-ABI
+    launches (no host overhead), and the same call through the Python API."""
     import torch
 
     x = torch.zeros(plan.n, dtype=torch.uint64, device="cuda")
+    q, mode, mu, s_in, s_out = plan.red_args
+    pairs, _ = nt.kernels._pairs_for(plan.tw_fwd, int(q))
+    log_n = plan.n.bit_length() - 1
+    side = torch.cuda.Stream()
+
+    def launch(st):
+        nt._lib.call("nttmul_ntt_ct", x.data_ptr(), pairs.data_ptr(), int(q), int(mode), int(mu),
+                     int(s_in), int(s_out), 0, log_n, 1, st)
+
+    res = {}
+    with torch.cuda.stream(side):
+        for _ in range(5):
+            launch(side.cuda_stream)
+        torch.cuda.synchronize()
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(20):
+                    launch(side.cuda_stream)
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(side)
+            for _ in range(10):
+                g.replay()
+            e1.record(side)
+            torch.cuda.synchronize()
+            res["device_us"] = round(e0.elapsed_time(e1) * 1e3 / 200, 2)
+        except Exception as exc:  # noqa: BLE001 - report, keep the API number
+            res["device_us"] = None
+            res["graph_error"] = str(exc)[:120]
     stream = torch.cuda.current_stream()
     for _ in range(5):
         nt.kernels.ntt_ct(x, plan.tw_fwd, *plan.red_args, False, None)
@@ -478,7 +558,8 @@ def ntt_latency_us(nt, plan):
         nt.kernels.ntt_ct(x, plan.tw_fwd, *plan.red_args, False, None)
     e1.record(stream)
     torch.cuda.synchronize()
-    return round(e0.elapsed_time(e1) * 1e3 / 50, 2)
+    res["api_us"] = round(e0.elapsed_time(e1) * 1e3 / 50, 2)
+    return res
 
 
 def run_reference(args, rank, world):

@@ -152,6 +152,9 @@ enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 #endif
 // issue a unit's twiddle loads before its data loads (hides their L2
 // latency; measured -2.7 % row-kernel time, sweep_r18)
+#ifndef NTTB_FWD_P_UNROLL
+#define NTTB_FWD_P_UNROLL 0
+#endif
 #ifndef NTTB_TW_PREFETCH
 #define NTTB_TW_PREFETCH 1
 #endif
@@ -212,7 +215,11 @@ __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
   using G = RowGeom<LOG_R>;
   constexpr int U = G::E >> R;         // units per thread
   constexpr int LK = LOG_R - S0 - R;   // log2(k_last)
+#if NTTB_FWD_P_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
   for (int p = 0; p < NP; ++p) {  // not unrolled: one polynomial's state live
     const u64 *__restrict__ g = p == 0 ? g0 : g1;
     u64 *__restrict__ s = sm + p * G::PADN;
