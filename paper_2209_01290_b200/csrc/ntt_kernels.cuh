@@ -712,14 +712,15 @@ struct ColParams {
 // sources, 4 stages) runs one column per thread with up to 128 registers;
 // the inverse pass (one source + folded scale) one column per thread at 4
 // CTAs per SM (64 registers).
-template <bool INV>
+template <bool INV, int LOG_N1 = 4>
 struct ColGeom {
   static constexpr int V = NTTB_COL_VEC;
-  static constexpr int MINB = INV ? NTTB_COL_MINB_INV : NTTB_COL_MINB;
+  // 32-word columns (n = 2^17) need the register budget of 2 CTAs/SM
+  static constexpr int MINB = LOG_N1 >= 5 ? 2 : (INV ? NTTB_COL_MINB_INV : NTTB_COL_MINB);
 };
 
 template <int LOG_N1, bool INV, int LB>
-__global__ void __launch_bounds__(COL_THREADS, ColGeom<INV>::MINB) col_kernel(const ColParams P) {
+__global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col_kernel(const ColParams P) {
   constexpr int N1 = 1 << LOG_N1;
   constexpr int V = ColGeom<INV>::V;
   const long long vecs = (P.npolys << COL_LOG_R) / V;  // column vectors per source
@@ -760,18 +761,39 @@ __global__ void __launch_bounds__(COL_THREADS, ColGeom<INV>::MINB) col_kernel(co
       x[0][e] = ldg_hint<L2_FIRST>(src + o);
     }
   }
-  if (!INV) {
 #if NTTB_COL_SMEM_TW
-    fwd_radix<LB, LOG_N1, LOG_N1, V>(x, 1, stw, M);
+  const ulonglong2 *twc = stw;
 #else
-    fwd_radix<LB, LOG_N1, LOG_N1, V>(x, 1, P.tw.fwd + limb * P.tw.stride, M);
+  const ulonglong2 *twc = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
 #endif
+  if constexpr (LOG_N1 == 5 && V == 1) {
+    // 32-row columns (n = 2^17): the stage whose pairs straddle the two
+    // 16-element halves runs on the whole column, the other four stages as
+    // two radix-16 units (B0 = 2 + h) - the single 5-stage unit is not
+    // register-promoted by the compiler (its 32-word array went to local
+    // memory).  Same butterflies, twiddles and reduction parity.
+    if (!INV) {
+      const ulonglong2 w = ldtw(twc, 1);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) ct_bfly<LB, true>(x[0][e], x[0][e + 16], w.x, w.y, M);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      u64 y[1][16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) y[0][e] = x[0][16 * h + e];
+      if (!INV)
+        fwd_radix<LB, 4, 4, 1, 1>(y, 2 + h, twc, M);
+      else
+        inv_radix<LB, 4, 4, 0, 1>(y, 2 + h, twc, M);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[0][16 * h + e] = y[0][e];
+    }
+    if (INV) inv_stage0<LB, LOG_N1, V>(x, 1, twc, L, M, P.fin);
+  } else if (!INV) {
+    fwd_radix<LB, LOG_N1, LOG_N1, V>(x, 1, twc, M);
   } else {
-#if NTTB_COL_SMEM_TW
-    const ulonglong2 *twi = stw;
-#else
-    const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
-#endif
+    const ulonglong2 *twi = twc;
     inv_radix<LB, LOG_N1, LOG_N1, 1, V>(x, 1, twi, M);
     inv_stage0<LB, LOG_N1, V>(x, 1, twi, L, M, P.fin);
   }
