@@ -152,6 +152,9 @@ enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 #endif
 // issue a unit's twiddle loads before its data loads (hides their L2
 // latency; measured -2.7 % row-kernel time, sweep_r18)
+#ifndef NTTB_B_OWN_COPIES
+#define NTTB_B_OWN_COPIES 1
+#endif
 #ifndef NTTB_FWD_P_UNROLL
 #define NTTB_FWD_P_UNROLL 0
 #endif
@@ -544,7 +547,11 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
     head_fwd<LB, LOG_R, 0, G::R(0), 1, true>(sm, P.in0 + off, nullptr, rowbase, twf, M);
     NTTB_STAMP(5);
     cp_async_wait<0>();
-    __syncthreads();
+    // Thread t copied exactly the words t + 512 k that its pass-0 unit of b
+    // reads (row_prefetch and head_fwd<S0 = 0> share the mapping), so its
+    // own wait_group makes them visible: no CTA barrier before b's pass 0.
+    if (!(NTTB_B_OWN_COPIES && G::R(0) == NTTB_ROW_LOG_E))
+      __syncthreads();
     NTTB_STAMP(1);
     head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sm + G::PADN, nullptr, nullptr, rowbase, twf, M);
     __syncthreads();
