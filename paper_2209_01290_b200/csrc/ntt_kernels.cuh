@@ -187,6 +187,35 @@ struct RowGeom {
   static_assert(NPASS >= 1 && NPASS <= 4, "row geometry");
 };
 
+// Swizzled index of element o0 + (e << LK) of a pass unit (o0 = the unit's
+// first element), with the XOR swizzle hoisted out of the element loop: for
+// strides of >= 8 rows (LK >= 7) the mask is the same for every element, so
+// the addresses are idx(o0) + immediate; for the 4-row stride of the middle
+// pass (LK = 6, unit start in rows 0-3 of an 8-row group) the mask flips by
+// f(4) = 12 on odd elements.  Other shapes use RowGeom::idx directly.
+#ifndef NTTB_SWZ_HOIST
+#define NTTB_SWZ_HOIST 1
+#endif
+template <int LOG_R, int LK>
+struct UnitIdx {
+  using G = RowGeom<LOG_R>;
+  static constexpr bool HOIST = NTTB_SWZ_HOIST && G::SWZ && LK >= 6;
+  int b0, b1;
+  __device__ __forceinline__ explicit UnitIdx(int o0) {
+    if constexpr (HOIST) {
+      b0 = G::idx(o0);
+      b1 = LK >= 7 ? b0 : (b0 ^ 12);
+    } else {
+      b0 = o0;
+      b1 = o0;
+    }
+  }
+  __device__ __forceinline__ int operator()(int e) const {
+    if constexpr (HOIST) return ((e & 1) ? b1 : b0) + (e << LK);
+    return G::idx(b0 + (e << LK));
+  }
+};
+
 struct RowParams {
   u64 *out;
   const u64 *in0;
@@ -235,11 +264,12 @@ __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
       TwBuf<0, R> twb;
       tw_prefetch(twb, tw, (rowbase << S0) + grp);
 #endif
+      const UnitIdx<LOG_R, LK> ix(o0);
       u64 x[1][1 << R];
 #pragma unroll
       for (int e = 0; e < (1 << R); ++e) {
         const int o = o0 + (e << LK);
-        x[0][e] = FROM_GLOBAL ? ldg_hint<L2_FIRST>(g + o) : s[G::idx(o)];
+        x[0][e] = FROM_GLOBAL ? ldg_hint<L2_FIRST>(g + o) : s[ix(e)];
       }
 #if NTTB_TW_PREFETCH
       fwd_radix_pf<LB, R, R, 1, S0 & 1>(x, twb, M);
@@ -247,7 +277,7 @@ __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
       fwd_radix<LB, R, R, 1, S0 & 1>(x, (rowbase << S0) + grp, tw, M);
 #endif
 #pragma unroll
-      for (int e = 0; e < (1 << R); ++e) s[G::idx(o0 + (e << LK))] = x[0][e];
+      for (int e = 0; e < (1 << R); ++e) s[ix(e)] = x[0][e];
     }
   }
 }
@@ -272,8 +302,9 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
     tw_prefetch(twb, tw, B0);
 #endif
     u64 x[1][1 << R];
+    const UnitIdx<LOG_R, LK> ix(o0);
 #pragma unroll
-    for (int e = 0; e < (1 << R); ++e) x[0][e] = sm[G::idx(o0 + (e << LK))];
+    for (int e = 0; e < (1 << R); ++e) x[0][e] = sm[ix(e)];
     if (TO_GLOBAL) {
 #if NTTB_TW_PREFETCH
       inv_radix_pf<LB, R, R, 1, 1>(x, twb, M);
@@ -290,7 +321,7 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
       inv_radix<LB, R, R, 0, 1>(x, B0, tw, M);
 #endif
 #pragma unroll
-      for (int e = 0; e < (1 << R); ++e) sm[G::idx(o0 + (e << LK))] = x[0][e];
+      for (int e = 0; e < (1 << R); ++e) sm[ix(e)] = x[0][e];
     }
   }
 }
