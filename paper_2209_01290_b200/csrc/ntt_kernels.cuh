@@ -194,24 +194,31 @@ struct RowGeom {
 // pass (LK = 6, unit start in rows 0-3 of an 8-row group) the mask flips by
 // f(4) = 12 on odd elements.  Other shapes use RowGeom::idx directly.
 #ifndef NTTB_SWZ_HOIST
-#define NTTB_SWZ_HOIST 1
+#define NTTB_SWZ_HOIST 2  // 1: the 8- and 4-row strides only; 2: also the 2-word stride and the tail
 #endif
+// For the 2-word stride of the last head pass (LK = 3, unit start in
+// words 0-7 of a 64-word block) element e sits in row 4g + e/2 at column
+// bit 3 = e & 1, so idx = (idx(o0) ^ (8 (e & 1) ^ e / 2)) + 16 (e / 2).
+// LK = 0 (the tail's 8 consecutive words, o0 = 8 t): idx = idx(o0) ^ e.
 template <int LOG_R, int LK>
 struct UnitIdx {
   using G = RowGeom<LOG_R>;
-  static constexpr bool HOIST = NTTB_SWZ_HOIST && G::SWZ && LK >= 6;
+  static constexpr bool HOIST =
+      NTTB_SWZ_HOIST && G::SWZ && (LK >= 6 || (NTTB_SWZ_HOIST > 1 && (LK == 3 || LK == 0)));
   int b0, b1;
   __device__ __forceinline__ explicit UnitIdx(int o0) {
     if constexpr (HOIST) {
       b0 = G::idx(o0);
-      b1 = LK >= 7 ? b0 : (b0 ^ 12);
+      b1 = LK == 6 ? (b0 ^ 12) : b0;
     } else {
       b0 = o0;
       b1 = o0;
     }
   }
   __device__ __forceinline__ int operator()(int e) const {
-    if constexpr (HOIST) return ((e & 1) ? b1 : b0) + (e << LK);
+    if constexpr (HOIST && LK >= 6) return ((e & 1) ? b1 : b0) + (e << LK);
+    if constexpr (HOIST && LK == 3) return (b0 ^ ((8 * (e & 1)) ^ (e >> 1))) + 16 * (e >> 1);
+    if constexpr (HOIST && LK == 0) return b0 ^ e;
     return G::idx(b0 + (e << LK));
   }
 };
@@ -405,8 +412,15 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int LOG_R>
 __device__ __forceinline__ void row_prefetch(u64 *__restrict__ dst, const u64 *__restrict__ src) {
   using G = RowGeom<LOG_R>;
+  if constexpr (G::SWZ && NTTB_SWZ_HOIST) {  // stride T = 512 words = 32 rows: same mask
+    const int b = G::idx(threadIdx.x);
 #pragma unroll
-  for (int i = threadIdx.x; i < G::N2; i += G::T) cp_async8(dst + G::idx(i), src + i);
+    for (int k = 0; k < G::N2 / G::T; ++k)
+      cp_async8(dst + b + k * G::T, src + threadIdx.x + k * G::T);
+  } else {
+#pragma unroll
+    for (int i = threadIdx.x; i < G::N2; i += G::T) cp_async8(dst + G::idx(i), src + i);
+  }
 }
 
 // all forward head passes of ONE polynomial already in smem `s`
@@ -441,9 +455,10 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   TwBuf<0, LE - 1> twb;
   if constexpr (MID) tw_prefetch(twb, twf, B0);
 #endif
+  const UnitIdx<LOG_R, 0> ix(o0);
   u64 xa[1][E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) xa[0][e] = sm[G::idx(o0 + e)];
+  for (int e = 0; e < E; ++e) xa[0][e] = sm[ix(e)];
   if constexpr (MID) {
     // a's last truncated stages first, parked (canonical) in its own smem
     // slots; then b's, kept in registers and overwritten by c pair by pair.
@@ -454,10 +469,10 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
 #endif
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      sm[G::idx(o0 + e)] =
+      sm[ix(e)] =
           LAZY_MID ? to2q_any<LB>(xa[0][e], M) : canon_fwd<LB>(xa[0][e], M);
 #pragma unroll
-    for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + G::idx(o0 + e)];
+    for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + ix(e)];
 #if NTTB_TW_PREFETCH
     fwd_radix_pf<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, twb, M);
     tw_prefetch(twb, twi, B0);  // inverse twiddles of the same groups
@@ -474,11 +489,11 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
       for (int h = 0; h < 2; ++h) {
         const int i0 = 2 * (p + h);
         if constexpr (LAZY_MID)
-          fused_pair_lazy<FAST, lb_pm<LB>()>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
+          fused_pair_lazy<FAST, lb_pm<LB>()>(sm[ix(i0)], sm[ix(i0 + 1)],
                                 to2q_any<LB>(xa[0][i0], M), to2q_any<LB>(xa[0][i0 + 1], M), w.x,
                                 w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
         else
-          fused_pair<MODE>(sm[G::idx(o0 + i0)], sm[G::idx(o0 + i0 + 1)],
+          fused_pair<MODE>(sm[ix(i0)], sm[ix(i0 + 1)],
                            canon_fwd<LB>(xa[0][i0], M), canon_fwd<LB>(xa[0][i0 + 1], M),
                            w.x, w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
       }
@@ -489,7 +504,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
     inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
 #endif
 #pragma unroll
-    for (int e = 0; e < E; ++e) sm[G::idx(o0 + e)] = xa[0][e];
+    for (int e = 0; e < E; ++e) sm[ix(e)] = xa[0][e];
   } else {
     static_assert(NP == 1, "unfused row passes transform one polynomial");
     if (FWD == FWD_FULL) fwd_radix<LB, LE, LE, 1, G::HEAD & 1>(xa, B0, twf, M);
@@ -501,7 +516,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
       for (int e = 0; e < E; ++e) xa[0][e] = canon_fwd<LB>(xa[0][e], M);
     }
 #pragma unroll
-    for (int e = 0; e < E; ++e) sm[G::idx(o0 + e)] = xa[0][e];
+    for (int e = 0; e < E; ++e) sm[ix(e)] = xa[0][e];
   }
 }
 
