@@ -333,6 +333,34 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
   }
 }
 
+// Pull the twiddle pairs the thread's unit of head pass I will read into L1
+// before the barrier that precedes the pass (no registers: prefetch.L1), so
+// the loads issued after the barrier hit L1 instead of waiting on L2.  Stage
+// t of the unit reads the 2^t consecutive pairs starting at (B0 << t).
+#ifndef NTTB_TW_L1PF
+#define NTTB_TW_L1PF 0  // measured +-0 (row 0.5289 ms both ways, r50): twiddle latency is not the limiter
+#endif
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+template <int R>
+__device__ __forceinline__ void tw_prefetch_l1(const ulonglong2 *tw, u64 B0) {
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    prefetch_l1(tw + (B0 << t));
+    if (t >= 3) prefetch_l1(tw + (B0 << t) + (1 << t) - 1);  // > 128 B range
+  }
+}
+template <int LOG_R, int I>
+__device__ __forceinline__ void pass_tw_l1(const ulonglong2 *tw, u64 rowbase) {
+  using G = RowGeom<LOG_R>;
+  if constexpr (NTTB_TW_L1PF && I < G::NPASS && (G::E >> G::R(I)) == 1) {
+    constexpr int LK = LOG_R - G::S0(I) - G::R(I);
+    const u64 B0 = (rowbase << G::S0(I)) + (threadIdx.x >> LK);
+    tw_prefetch_l1<G::R(I)>(tw, B0);
+  }
+}
+
 // Barrier between two row passes.  A pass with first stage S0 transforms
 // independent blocks of 2^(LOG_R - S0) elements; when every pass gives each
 // thread one unit (R == LOG_E), the threads that own a block are the
@@ -368,6 +396,12 @@ __device__ __forceinline__ void head_fwd_all(u64 *sm, const u64 *g0, const u64 *
   using G = RowGeom<LOG_R>;
   if constexpr (I < G::NPASS) {
     head_fwd<LB, LOG_R, G::S0(I), G::R(I), NP, I == 0>(sm, g0, g1, rowbase, tw, M);
+    pass_tw_l1<LOG_R, I + 1>(tw, rowbase);
+    if constexpr (NTTB_TW_L1PF && I + 1 == G::NPASS && G::HEAD > 0) {
+      // the tail's forward stage twiddles (its inverse ones come from the
+      // other table, prefetched by the caller's tail)
+      tw_prefetch_l1<(LOG_R - G::HEAD) - 1>(tw, (rowbase << G::HEAD) + threadIdx.x);
+    }
     row_sync<LOG_R, G::S0(I)>();
     if (I == 0) NTTB_STAMP(1);
     head_fwd_all<LB, LOG_R, NP, I + 1>(sm, g0, g1, rowbase, tw, M);
@@ -383,6 +417,7 @@ __device__ __forceinline__ void head_inv_all(u64 *sm, u64 *gout, u64 rowbase,
   if constexpr (I > 0) {
     head_inv<LB, LOG_R, G::S0(I), G::R(I), false>(sm, nullptr, rowbase, tw, L, M,
                                                   FIN_LAZY);
+    pass_tw_l1<LOG_R, I - 1>(tw, rowbase);
     row_sync<LOG_R, G::S0(I - 1)>();
     head_inv_all<LB, LOG_R, I - 1>(sm, gout, rowbase, tw, L, M, fin);
   } else {
@@ -600,6 +635,7 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
       __syncthreads();
     NTTB_STAMP(1);
     head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sm + G::PADN, nullptr, nullptr, rowbase, twf, M);
+    pass_tw_l1<LOG_R, 1>(twf, rowbase);
     __syncthreads();
     NTTB_STAMP(6);
     head_fwd_all<LB, LOG_R, NP, 1>(sm, nullptr, nullptr, rowbase, twf, M);
@@ -625,6 +661,7 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
   }
   NTTB_STAMP(2);
   tail_pass<LB, LOG_R, NP, FWD, MID, INV, MODE>(sm, rowbase, twf, twi, L, M);
+  if (INV != INV_NONE || MID) pass_tw_l1<LOG_R, G::NPASS - 1>(twi, rowbase);
   if (INV != INV_NONE || MID)
     row_sync<LOG_R, G::S0(G::NPASS - 1)>();  // the inverse passes read back this tail
   else
