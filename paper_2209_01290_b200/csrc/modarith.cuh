@@ -103,6 +103,10 @@ __device__ __forceinline__ u64 pack(uint32_t lo, uint32_t hi) {
   return r;
 }
 
+#ifndef NTTB_LB32_STAGES
+#define NTTB_LB32_STAGES 0  // 1: multiply-reduced stage schedule (measured slower: row 0.574 vs 0.551 ms, sweep_r35)
+#endif
+
 // Per-prime constants the butterflies need.
 struct Mod {
   u64 q, q2, q4, q8;
@@ -175,6 +179,17 @@ __device__ __forceinline__ Mod mod_for(u64 q) {
 }
 template <int LB>
 __host__ __device__ constexpr bool lb_pm() { return LB == 33; }
+
+// Constants for kernels that run transform stages only (no fused middle):
+// the multiply-based reduction constants are needed there only with the
+// multiply-reduced stage schedule, so skip their double division.
+template <int LB>
+__device__ __forceinline__ Mod mod_for_stages(u64 q) {
+  Mod m = (LB >= 32 && NTTB_LB32_STAGES) ? make_mod_fast(q) : make_mod(q);
+  if (LB == 33 && !NTTB_LB32_STAGES)
+    m.ps = static_cast<uint32_t>(__ffs(static_cast<int>(0u - m.nqh)) - 1);
+  return m;
+}
 
 template <bool PM = false>
 __device__ __forceinline__ u64 reduce2q(u64 x, const Mod &M) {
@@ -278,9 +293,6 @@ __device__ __forceinline__ u64 mulred_lazy(u64 a, u64 b, const Limb &L, const Mo
 // LB = 16 (moduli < 2^60) alternates reducing (RED) and non-reducing stages:
 // a RED stage takes X < 16q to [0, 8q) and emits < 12q, the next stage
 // skips the correction and emits < 16q - half the forward corrections.
-#ifndef NTTB_LB32_STAGES
-#define NTTB_LB32_STAGES 0  // 1: multiply-reduced stage schedule (measured slower: row 0.574 vs 0.551 ms, sweep_r35)
-#endif
 
 template <int LB, bool RED = true>
 __device__ __forceinline__ void ct_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod &M) {

@@ -41,7 +41,10 @@ struct LimbSet {
 // struct lives in kernel-parameter space)
 __device__ __forceinline__ const Limb *limb_ptr(const LimbSet &S, long long poly, int &limb) {
   if (S.table) {
-    limb = static_cast<int>((poly + S.base) % S.num);
+    // 32-bit remainder (a 64-bit one is a long emulated sequence); poly
+    // indices of one launch stay far below 2^32 (each is >= 4 KiB of HBM)
+    limb = static_cast<int>((static_cast<unsigned>(poly) + static_cast<unsigned>(S.base)) %
+                            static_cast<unsigned>(S.num));
     return S.table + limb;
   }
   limb = 0;
@@ -814,17 +817,19 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
   constexpr int N1 = 1 << LOG_N1;
   constexpr int V = ColGeom<INV>::V;
   const long long vecs = (P.npolys << COL_LOG_R) / V;  // column vectors per source
-  const long long gid = blockIdx.x * static_cast<long long>(COL_THREADS) +
-                        threadIdx.x;
-  if (gid >= vecs * P.nsrc) return;
-  const int which = gid >= vecs ? 1 : 0;
-  const long long rem = (gid - (which ? vecs : 0)) * V;  // first column (global)
-  const long long poly = rem >> COL_LOG_R;
+  // a CTA's COL_THREADS * V columns lie in one polynomial of one source
+  // (4096 columns per polynomial), so source, polynomial and limb are
+  // CTA-uniform: derive them from blockIdx only
+  const long long cta0 = blockIdx.x * static_cast<long long>(COL_THREADS);
+  if (cta0 >= vecs * P.nsrc) return;
+  const int which = cta0 >= vecs ? 1 : 0;
+  const long long rem = (cta0 - (which ? vecs : 0)) * V + threadIdx.x * V;  // first column
+  const long long poly = ((cta0 - (which ? vecs : 0)) * V) >> COL_LOG_R;
   const long long base =
       (poly << (COL_LOG_R + LOG_N1)) + (rem & ((1 << COL_LOG_R) - 1));
   int limb;
   const Limb &L = *limb_ptr(P.limbs, poly, limb);
-  const Mod M = mod_for<LB>(L.q);
+  const Mod M = mod_for_stages<LB>(L.q);
   const u64 *__restrict__ src = (which ? P.src1 : P.src0) + base;
   u64 *__restrict__ dst = (which ? P.dst1 : P.dst0) + base;
 #if NTTB_COL_SMEM_TW
@@ -1026,7 +1031,7 @@ __global__ void __launch_bounds__(ColPipeGeom<LOG_N1>::TC)
     where(t, which, poly, col0);
     int limb;
     const Limb &L = *limb_ptr(P.limbs, poly, limb);
-    const Mod M = mod_for<LB>(L.q);
+    const Mod M = mod_for_stages<LB>(L.q);
     u64 *buf = csm + s * G::TILE_WORDS;
     bulk::mbar_wait(bars + s, (it / S) & 1);
     u64 x[1][N1];
@@ -1130,7 +1135,7 @@ __device__ __noinline__ void group_phase1(const GroupParams &P, long long p, int
   constexpr long long N = static_cast<long long>(N1) * N2;
   int limb;
   const Limb &L = *limb_ptr(P.limbs, p, limb);
-  const Mod M = mod_for<LB>(L.q);
+  const Mod M = mod_for_stages<LB>(L.q);
   const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
 #pragma unroll 1
   for (int j = threadIdx.x; j < 2 * SW; j += blockDim.x) {
@@ -1185,7 +1190,7 @@ __device__ __noinline__ void group_phase3(const GroupParams &P, long long p, int
   constexpr long long N = static_cast<long long>(N1) * N2;
   int limb;
   const Limb &L = *limb_ptr(P.limbs, p, limb);
-  const Mod M = mod_for<LB>(L.q);
+  const Mod M = mod_for_stages<LB>(L.q);
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
 #pragma unroll 1
   for (int j = threadIdx.x; j < SW; j += blockDim.x) {
