@@ -27,6 +27,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+CFG_NAMES = {(16, 21): "cfg3", (14, 8): "cfg2", (17, 32): "cfg4", (12, 1): "cfg1"}
 METRIC = "polymuls/sec at N=2^16×21 limbs; NTT µs; % of HBM/int-pipe roofline"
 UNIT = "ct-polymul/s"
 
@@ -362,8 +363,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic uniform residues (numpy default_rng), "
-                                   "primes/psi = reference RnsBasis.build(65536, 60, 21, seed=0)",
-            "config": {"workload": f"cfg3: fused negacyclic polymul, N=2^{args.log_n}, "
+                                   f"primes/psi = reference RnsBasis.build({n}, 60, {L}, seed=0)",
+            "config": {"workload": f"{CFG_NAMES.get((args.log_n, L), 'custom')}: fused "
+                                   f"negacyclic polymul, N=2^{args.log_n}, "
                                    f"{L} x 60-bit RNS limbs",
                        "batch_per_gpu": Bn, "global_batch": Bn * world, "n": n, "limbs": L,
                        "parallelism": f"shard-by-ciphertext x{world}",
@@ -601,7 +603,8 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 / value, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic uniform residues",
-            "config": {"workload": f"cfg3: fused negacyclic polymul, N=2^{args.log_n}, "
+            "config": {"workload": f"{CFG_NAMES.get((args.log_n, L), 'custom')}: fused "
+                                   f"negacyclic polymul, N=2^{args.log_n}, "
                                    f"{L} x 60-bit RNS limbs", "n": n, "limbs": L},
             "impl": "reference",
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
