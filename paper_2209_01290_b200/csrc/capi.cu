@@ -465,6 +465,9 @@ int run_polymul_one(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *w
 #ifndef NTTB_SPLIT_STREAMS
 #define NTTB_SPLIT_STREAMS 2
 #endif
+#ifndef NTTB_SPLIT_STAGGER
+#define NTTB_SPLIT_STAGGER 1
+#endif
 #ifndef NTTB_SPLIT_PARTS
 #define NTTB_SPLIT_PARTS NTTB_SPLIT_STREAMS  // parts, assigned round-robin to the streams
 #endif
@@ -478,7 +481,7 @@ int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
     return run_polymul_one(mode, lb, c, a, b, ws, tw, ls, log_n, npolys, phases, st);
   struct Side {
     cudaStream_t s[K];
-    cudaEvent_t fork, join[K];
+    cudaEvent_t fork, join[K], stag[NP];
   };
   static Side sides[64];
   int dev = 0;
@@ -491,6 +494,9 @@ int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
       if (cudaStreamCreateWithFlags(&sd.s[k], cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&sd.join[k], cudaEventDisableTiming) != cudaSuccess)
         return cuda_status("split streams");
+    for (int p = 0; p < NP; ++p)
+      if (cudaEventCreateWithFlags(&sd.stag[p], cudaEventDisableTiming) != cudaSuccess)
+        return cuda_status("split streams");
   }
   if (cudaEventRecord(sd.fork, st) != cudaSuccess) return cuda_status("split fork");
   const long long n = 1LL << log_n;
@@ -501,8 +507,22 @@ int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
     const long long cnt = (npolys - off) / (NP - p);
     LimbSet lk = ls;
     lk.base = static_cast<int>((ls.base + off) % (ls.num > 0 ? ls.num : 1));
-    CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw, lk,
-                          log_n, cnt, phases, sd.s[p % K]));
+    cudaStream_t sp = sd.s[p % K];
+    if (NTTB_SPLIT_STAGGER) {
+      // part p's forward columns start once part p-1's are done, so they
+      // run beside part p-1's row kernel instead of all parts' columns
+      // competing for HBM at the start
+      if (p > 0 && cudaStreamWaitEvent(sp, sd.stag[p - 1]) != cudaSuccess)
+        return cuda_status("split stagger");
+      CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw,
+                            lk, log_n, cnt, phases & 1, sp));
+      if (cudaEventRecord(sd.stag[p], sp) != cudaSuccess) return cuda_status("split stagger");
+      CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw,
+                            lk, log_n, cnt, phases & 6, sp));
+    } else {
+      CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw,
+                            lk, log_n, cnt, phases, sp));
+    }
     off += cnt;
   }
   for (int k = 0; k < K; ++k)
