@@ -249,9 +249,19 @@ def main():
 
     import paper_2209_01290_b200 as nt
 
+    # NTTB_BENCH_SHARE_GPU=1 (tests of the N>1 logic on a 1-GPU box only):
+    # ranks share the visible GPUs round-robin and talk over gloo, since NCCL
+    # refuses two ranks on one device.  Never set for a measured run.
+    share = os.environ.get("NTTB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if share else "cuda"
     n, L, Bn = 1 << args.log_n, args.limbs, args.batch
     basis = nt.RnsBasis.build(n, 60, L, seed=0)
     primes = list(basis.primes)
@@ -308,7 +318,7 @@ def main():
             phase_ms[nm] = phase_ms.get(nm, 0.0) + evs[k][0].elapsed_time(evs[k][1])
     phase_ms = {k: v / args.steps for k, v in phase_ms.items()}
 
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -403,7 +413,8 @@ def run_e2e(nt, basis, A_h, B_h, args, world, stream, C_dev):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    share = os.environ.get("NTTB_BENCH_SHARE_GPU") == "1"
+    t = torch.tensor([ms], dtype=torch.float64, device="cpu" if share else "cuda")
     if world > 1:
         import torch.distributed as dist
 
