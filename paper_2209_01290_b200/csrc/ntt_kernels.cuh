@@ -596,6 +596,33 @@ __device__ __forceinline__ void tail_pass_split(u64 *__restrict__ sa, u64 *__res
   for (int e = 0; e < E; ++e) sa[G::idx(o0 + e)] = xa[0][e];
 }
 
+// Split CTA barrier (mbarrier): every thread arrives as soon as its writes
+// are done and waits only where it needs the other threads' data, so the
+// work placed between arrive and wait hides the barrier.
+#ifndef NTTB_SPLIT_BAR
+#define NTTB_SPLIT_BAR 1
+#endif
+__device__ __forceinline__ void sbar_init(u64 *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void sbar_arrive(u64 *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void sbar_wait(u64 *bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "SBAR_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SBAR_WAIT_%=;\n\t}" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+      "r"(parity)
+      : "memory");
+}
+
 template <int LOG_R, int FWD, bool MID, int INV, int MODE, int LB>
 __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
                                   MID ? NTTB_ROW_MINB_FUSED : NTTB_ROW_MINB)
@@ -623,7 +650,41 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
     if (NP > 1) prefetch_l2(P.in1 + nx, G::N2 * sizeof(u64));
   }
 
-  if (MID && NTTB_PREFETCH_B) {
+  constexpr bool SPLIT = NTTB_SPLIT_BAR && NTTB_B_OWN_COPIES && G::R(0) == NTTB_ROW_LOG_E &&
+                        G::NPASS >= 2;
+  __shared__ u64 sbar[2];  // SPLIT: a's / b's first pass written
+  if (MID && NTTB_PREFETCH_B && SPLIT) {
+    // b's row streams into its smem slot (cp.async, each thread exactly the
+    // words its own first-pass unit reads) while a's first pass loads and
+    // transforms a.  The CTA-wide dependency pass 0 -> pass 1 is split per
+    // polynomial: arrive after a's pass 0, b's pass 0, wait(a), a's pass 1,
+    // wait(b), b's pass 1 - the waits are mostly satisfied by then.
+    if (threadIdx.x == 0) {
+      sbar_init(&sbar[0], G::T);
+      sbar_init(&sbar[1], G::T);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    row_prefetch<LOG_R>(sm + G::PADN, P.in1 + off);
+    cp_async_commit();
+    __syncthreads();  // barrier init visible (all threads are at the start)
+    head_fwd<LB, LOG_R, 0, G::R(0), 1, true>(sm, P.in0 + off, nullptr, rowbase, twf, M);
+    sbar_arrive(&sbar[0]);
+    cp_async_wait<0>();
+    head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sm + G::PADN, nullptr, nullptr, rowbase, twf, M);
+    sbar_arrive(&sbar[1]);
+    sbar_wait(&sbar[0], 0);
+    head_fwd<LB, LOG_R, G::S0(1), G::R(1), 1, false>(sm, nullptr, nullptr, rowbase, twf, M);
+    sbar_wait(&sbar[1], 0);
+    head_fwd<LB, LOG_R, G::S0(1), G::R(1), 1, false>(sm + G::PADN, nullptr, nullptr, rowbase,
+                                                     twf, M);
+    row_sync<LOG_R, G::S0(1)>();
+    head_fwd_all<LB, LOG_R, NP, 2>(sm, nullptr, nullptr, rowbase, twf, M);
+    if (P.discard_in) {
+      constexpr int LINES = G::N2 * 8 / 128;
+      for (int i = threadIdx.x; i < NP * LINES; i += G::T)
+        discard_line((i < LINES ? P.in0 : P.in1) + off + (i % LINES) * 16);
+    }
+  } else if (MID && NTTB_PREFETCH_B) {
     // b's row streams into its smem slot (cp.async) while a's first pass
     // loads and transforms a; then b's first pass runs from smem.
     row_prefetch<LOG_R>(sm + G::PADN, P.in1 + off);
