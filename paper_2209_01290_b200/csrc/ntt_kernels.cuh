@@ -838,6 +838,9 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T, NTTB_ROW_MINB_FUSED)
 #ifndef NTTB_COL_MINB
 #define NTTB_COL_MINB 4  // forward columns at 4 CTAs/SM (64 regs) since the loads go out first: col fwd 0.145 -> 0.123 ms (sweep_r60)
 #endif
+#ifndef NTTB_COL_INV_LOADS_FIRST
+#define NTTB_COL_INV_LOADS_FIRST 0
+#endif
 #ifndef NTTB_COL_MINB_INV
 #define NTTB_COL_MINB_INV 3
 #endif
@@ -906,7 +909,7 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
     if (threadIdx.x < N1) stw[threadIdx.x] = tg[threadIdx.x];
     __syncthreads();
   };
-  if (INV) stage_tw();
+  if (INV && !NTTB_COL_INV_LOADS_FIRST) stage_tw();
 #endif
   u64 x[V][N1];
 #pragma unroll
@@ -921,7 +924,7 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
     }
   }
 #if NTTB_COL_SMEM_TW
-  if (!INV) stage_tw();
+  if (!INV || NTTB_COL_INV_LOADS_FIRST) stage_tw();
 #endif
 #if NTTB_COL_SMEM_TW
   const ulonglong2 *twc = stw;
