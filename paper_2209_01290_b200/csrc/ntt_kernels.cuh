@@ -839,10 +839,10 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T, NTTB_ROW_MINB_FUSED)
 #define NTTB_COL_MINB 4  // forward columns at 4 CTAs/SM (64 regs) since the loads go out first: col fwd 0.145 -> 0.123 ms (sweep_r60)
 #endif
 #ifndef NTTB_COL_INV_LOADS_FIRST
-#define NTTB_COL_INV_LOADS_FIRST 0
+#define NTTB_COL_INV_LOADS_FIRST 1  // with 4 CTAs/SM: col inv 0.0803 -> 0.0763 ms (sweep_r62)
 #endif
 #ifndef NTTB_COL_MINB_INV
-#define NTTB_COL_MINB_INV 3
+#define NTTB_COL_MINB_INV 4
 #endif
 constexpr int COL_LOG_R = NTTB_COL_LOG_R;  // row length used for n > 2^COL_LOG_R
 constexpr int COL_THREADS = 256;
@@ -900,9 +900,9 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
   // The N1 - 1 column twiddles are the same for the whole CTA (its 256
   // columns lie in one polynomial): stage them in shared memory so the
   // butterflies read them just in time (LDS broadcast) instead of the
-  // compiler hoisting 2 x (N1 - 1) global loads into registers.  Forward:
-  // the column loads go out first and the staging barrier overlaps their
-  // HBM latency (-4 %); inverse: staging first measured faster (+2 % else).
+  // compiler hoisting 2 x (N1 - 1) global loads into registers.  The
+  // column loads go out first and the staging barrier overlaps their HBM
+  // latency (forward -4 %, then 4 CTAs/SM -15 %; inverse at 4 CTAs/SM -5 %).
   __shared__ ulonglong2 stw[N1];
   auto stage_tw = [&] {
     const ulonglong2 *tg = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
