@@ -45,8 +45,6 @@ def parse():
                     help="target CPU work for the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--pipeline", default=None,
-                    help="chunk_ciphertexts,streams for nttmul_set_pipeline")
     return ap.parse_args()
 
 
@@ -275,9 +273,6 @@ def main():
     fwd, inv, limbs = basis.device_tables()
     stream = torch.cuda.current_stream()
     lib = nt._lib
-    if args.pipeline:
-        chunk, nstreams = (int(x) for x in args.pipeline.split(","))
-        lib.call("nttmul_set_pipeline", chunk, nstreams)
 
     def step(phases=7):
         lib.call("nttmul_polymul_fused_rns_phases", C.data_ptr(), A.data_ptr(), B.data_ptr(),
@@ -437,9 +432,6 @@ def modmul_roof(nt, basis, stream):
     limb = basis.plans[0].limb()
     sink = torch.zeros(1, dtype=torch.uint64, device="cuda")
     best = {}
-    # the forms the default fused schedule runs (the LB = 32 stage forms,
-    # kinds 4/5, and the shift-shaped-modulus forms, kinds 6/7, belong to
-    # opt-in schedules: NTTB_LB32_STAGES / NTTB_PM_SHIFT)
     kinds = [(1, "shoup"), (0, "barrett_proposed"), (2, "ct_butterfly"), (3, "gs_butterfly")]
     for kind, label in kinds:
         cnt = ctypes.c_double()

@@ -61,11 +61,8 @@ extern "C" {
  * bits: the fused product's middle then uses multiply-based partial
  * reductions instead of conditional-subtraction chains. */
 #define NTTMUL_MODE_WIDE35 0x400
-/* OR-ed in (with NTTMUL_MODE_WIDE35) when EVERY modulus q is "shift-shaped":
- * hi32(2^64 - q) = 2^32 - 2^s for some s, i.e. q lies in
- * [2^(32+s) - 2^32, 2^(32+s)) (e.g. the 60-bit NTT primes 2^60 - delta,
- * delta < 2^32, that RnsBasis.build returns).  Products by the high word of
- * -q then become shifts.  Setting it for other moduli gives wrong results. */
+/* Accepted and ignored (ABI 1 compatibility): the shift-shaped-modulus
+ * schedule it selected measured slower and was removed. */
 #define NTTMUL_MODE_PM 0x800
 
 /* largest supported transform: n = 2^17 (BASELINE cfg4) */
@@ -249,15 +246,6 @@ int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
                                   uint64_t *dev_buf, int64_t chunk_cts,
                                   void *stream);
 
-/*
- * Pipeline knob of nttmul_polymul_fused_rns for n > 4096 (process-wide):
- * the batch is processed in chunks of `chunk_waves` fused-row-kernel waves
- * whose intermediates stay in L2 (scratch lines are discarded once read, so
- * only a, b and c touch HBM).  chunk_waves = 0 runs the whole batch as one
- * column / row / column sequence through HBM.  `reserved` must be >= 0.
- */
-int nttmul_set_pipeline(int chunk_waves, int reserved);
-
 /* ---- RNS decomposition / CRT reconstruction (rns.py:82-108) ------------- */
 
 /*
@@ -319,15 +307,6 @@ int nttmul_sweep_exhaustive(uint64_t q_lo, uint64_t q_hi, uint64_t *tallies,
 int nttmul_gather(uint64_t *out, const uint64_t *in, const int64_t *idx,
                   int64_t n, int64_t batch, void *stream);
 
-/*
- * Schedule knob of nttmul_polymul_fused_rns for n > 4096 (process-wide):
- * enable = 1 runs large batches (>= 4 products per group) as ONE cooperative
- * group-persistent launch whose intermediates stay in L2; enable = 0
- * (default, measured faster) uses the three-launch column / row / column
- * pipeline.  Both give identical results.
- */
-int nttmul_set_group(int enable);
-
 /* ---- measurement --------------------------------------------------------- */
 
 /*
@@ -335,11 +314,8 @@ int nttmul_set_group(int enable);
  * every thread runs `iters` iterations of `chains` independent dependent
  * modmul chains.  kind 0 = Barrett data*data (mode from limb), 1 = Shoup
  * (fixed multiplicand), 2 = lazy forward CT butterfly, 3 = lazy inverse GS
- * butterfly (kinds 2/3 count one modmul per butterfly; need q < 2^61),
- * 4 / 5 = the forward / inverse butterflies of the multiply-reduced LB = 32
- * schedule (reduce-plain-plain / reduce-plain; need a 35..60-bit q),
- * 6 / 7 = the forward / inverse butterflies for shift-shaped moduli
- * (NTTMUL_MODE_PM; reduce-plain).  Writes an XOR sink to *sink_out so the
+ * butterfly (kinds 2/3 count one modmul per butterfly; need q < 2^61).
+ * Writes an XOR sink to *sink_out so the
  * work cannot be elided.  Returns the number of modmuls issued in *modmuls_out (host).
  */
 int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks,

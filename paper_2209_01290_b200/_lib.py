@@ -13,7 +13,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "libnttmul_b200.so"
-LIB_PATH = os.path.join(HERE, LIB_NAME)
+# NTTMUL_LIB: an alternative build of the same ABI (A/B measurements only)
+LIB_PATH = os.environ.get("NTTMUL_LIB") or os.path.join(HERE, LIB_NAME)
 
 ABI_VERSION = 1
 
@@ -72,8 +73,6 @@ _PROTOS = {
                                                  _c_i64, _c_int, _vp, _c_int, _vp]),
     "nttmul_polymul_fused_rns_host": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                                _c_i64, _c_int, _vp, _c_i64, _vp]),
-    "nttmul_set_pipeline": (_c_int, [_c_int, _c_int]),
-    "nttmul_set_group": (_c_int, [_c_int]),
     "nttmul_negacyclic_naive": (_c_int, [_vp, _vp, _vp, _c_u64, _c_i64, _c_i64, _vp]),
     "nttmul_sweep_random": (_c_int, [_c_int, _c_u64, _c_u64, _vp, _vp, _vp]),
     "nttmul_sweep_exhaustive": (_c_int, [_c_u64, _c_u64, _vp, _vp, _vp]),

@@ -94,13 +94,7 @@ int smem_optin(K kernel, size_t bytes) {
 template <int LOG_R, int FWD, bool MID, int INV, int MODE, int LB>
 int launch_row_t(const RowParams &P, long long rows, cudaStream_t st) {
   constexpr int NP = MID ? 2 : 1;
-  // NTTB_ROW_EXTRA_SMEM (bytes, experiments only): pad the dynamic shared
-  // memory to force fewer resident CTAs per SM
-  static const size_t extra = [] {
-    const char *e = std::getenv("NTTB_ROW_EXTRA_SMEM");
-    return e ? static_cast<size_t>(std::atol(e)) : size_t(0);
-  }();
-  const size_t smem = NP * RowGeom<LOG_R>::PADN * sizeof(u64) + extra;
+  const size_t smem = NP * RowGeom<LOG_R>::PADN * sizeof(u64);
   auto k = row_kernel<LOG_R, FWD, MID, INV, MODE, LB>;
   CHECK(smem_optin(k, smem));
   static long long slots = 0;  // resident CTAs per device for this instantiation
@@ -135,91 +129,23 @@ int launch_row_m(int log_r, const RowParams &P, long long rows, cudaStream_t st)
   return fail(NTTMUL_EINVAL, "row size 2^%d unsupported", log_r);
 }
 
-// ---- persistent fused row kernel -------------------------------------------
-#ifndef NTTB_PERSISTENT
-#define NTTB_PERSISTENT 0  // 1: pipelined persistent fused row kernel (measured 0.622 vs 0.572 ms, sweep_r29)
-#endif
-template <int LOG_R, int MODE, int LB>
-int launch_row_persistent_t(const RowParams &P, long long rows, cudaStream_t st) {
-  const size_t smem = 2 * RowGeom<LOG_R>::PADN * sizeof(u64);
-  auto k = row_fused_persistent<LOG_R, MODE, LB>;
-  CHECK(smem_optin(k, smem));
-  static int slots = 0;  // resident CTAs per device for this instantiation
-  if (!slots) {
-    int dev = 0, sms = 148, nb = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, RowGeom<LOG_R>::T, smem) !=
-            cudaSuccess || nb < 1) {
-      cudaGetLastError();
-      nb = 1;
-    }
-    slots = nb * sms;
-  }
-  const long long grid = rows < slots ? rows : slots;
-  k<<<static_cast<unsigned>(grid), RowGeom<LOG_R>::T, smem, st>>>(P, rows);
-  return cuda_status("row_fused_persistent");
-}
-
+// ---- fused row kernel ---------------------------------------------------------
 template <int MODE, int LB>
 int launch_row_fused(int log_r, const RowParams &P, long long rows, cudaStream_t st) {
-  // the pipelined persistent kernel for the 4096-word rows of n > 4096
-  // (pipeline chunking, with its scratch discards, keeps the plain kernel)
-  if (NTTB_PERSISTENT && log_r == 12 && !P.discard_in)
-    return launch_row_persistent_t<12, MODE, LB>(P, rows, st);
   return launch_row_m<FWD_TRUNC, true, INV_SKIP, MODE, LB>(log_r, P, rows, st);
 }
 
 // ---- column kernel dispatch -------------------------------------------------
-#ifndef NTTB_COL_PIPE
-#define NTTB_COL_PIPE 0  // 1: bulk-copy pipelined column kernel (measured no faster, sweep_r16)
-#endif
-template <int LOG_N1, bool INV, int LB>
-int launch_col_pipe_t(const ColParams &P, cudaStream_t st) {
-  using G = ColPipeGeom<LOG_N1>;
-  auto k = col_pipe_kernel<LOG_N1, INV, LB>;
-  CHECK(smem_optin(k, G::SMEM));
-  static int slots = 0;  // resident CTAs per device for this instantiation
-  if (!slots) {
-    int dev = 0, sms = 148, nb = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, G::TC, G::SMEM) != cudaSuccess ||
-        nb < 1) {
-      cudaGetLastError();
-      nb = 1;
-    }
-    slots = nb * sms;
-  }
-  const long long tiles = P.nsrc * P.npolys * G::TILES_PER_POLY;
-  const long long grid = tiles < slots ? tiles : slots;
-  if (grid == 0) return NTTMUL_OK;
-  k<<<static_cast<unsigned>(grid), G::TC, G::SMEM, st>>>(P);
-  return cuda_status("col_pipe_kernel");
-}
-
 template <bool INV, int LB>
 int launch_col(int log_n1, const ColParams &P, cudaStream_t st) {
-  if (NTTB_COL_PIPE && !P.discard_src && COL_LOG_R == 12) {
-    switch (log_n1) {
-      case 1: return launch_col_pipe_t<1, INV, LB>(P, st);
-      case 2: return launch_col_pipe_t<2, INV, LB>(P, st);
-      case 3: return launch_col_pipe_t<3, INV, LB>(P, st);
-      case 4: return launch_col_pipe_t<4, INV, LB>(P, st);
-      case 5: return launch_col_pipe_t<5, INV, LB>(P, st);
-    }
-  }
   const unsigned grid = static_cast<unsigned>(
-      (P.nsrc * ((P.npolys << COL_LOG_R) / COL_VEC) + COL_THREADS - 1) / COL_THREADS);
+      (P.nsrc * (P.npolys << COL_LOG_R) + COL_THREADS - 1) / COL_THREADS);
   switch (log_n1) {
     case 1: col_kernel<1, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
     case 2: col_kernel<2, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
     case 3: col_kernel<3, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
     case 4: col_kernel<4, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
     case 5: col_kernel<5, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
-#if NTTB_COL_LOG_R < 12
-    case 6: col_kernel<6, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
-#endif
     default: return fail(NTTMUL_EINVAL, "column count 2^%d unsupported", log_n1);
   }
   return cuda_status("col_kernel");
@@ -257,7 +183,7 @@ int run_forward(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
   const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
   const int log_n1 = log_n - log_r;
   if (log_n1 > 0) {
-    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, FIN_LAZY, 0};
+    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, FIN_LAZY};
     CHECK((launch_col<false, LB>(log_n1, C, st)));
   }
   RowParams R{a, a, nullptr, tw, ls, log_n1, FIN_PLAIN, 0};
@@ -282,122 +208,19 @@ int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
   CHECK((skip ? launch_row_m<FWD_NONE, false, INV_SKIP, 2, LB>(log_r, R, rows, st)
               : launch_row_m<FWD_NONE, false, INV_FULL, 2, LB>(log_r, R, rows, st)));
   if (log_n1 > 0) {
-    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, fin, 0};
+    ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, fin};
     CHECK((launch_col<true, LB>(log_n1, C, st)));
   }
   return NTTMUL_OK;
 }
 
-// Row-kernel occupancy (CTAs per SM x SMs) of one instantiation - used to
-// size pipeline chunks in whole waves.
-template <int LOG_R, int MODE, int LB>
-long long fused_rows_per_wave() {
-  static long long cached = 0;
-  if (cached) return cached;
-  int dev = 0, sms = 148, nb = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  auto k = row_kernel<LOG_R, FWD_TRUNC, true, INV_SKIP, MODE, LB>;
-  const size_t smem = 2 * RowGeom<LOG_R>::PADN * sizeof(u64);
-  smem_optin(k, smem);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, RowGeom<LOG_R>::T, smem) !=
-          cudaSuccess || nb < 1) {
-    cudaGetLastError();
-    nb = 1;
-  }
-  cached = static_cast<long long>(nb) * sms;
-  return cached;
-}
-
-int g_chunk_waves = 0;  // row-kernel waves per pipeline chunk (0: no chunking; measured slower)
-
-#ifndef NTTB_GROUP
-// 1: one cooperative group-persistent launch for n > 4096 (phases == 7).
-// Measured slower than the three launches (1.13 vs 0.85 ms per cfg3 step,
-// profiles/r1/group_timing.txt): every phase already runs at the SM's
-// integer throughput, so keeping the intermediates in L2 saves nothing while
-// the column phases lose half their threads and the group barriers add waits.
-#define NTTB_GROUP 0
-#endif
-int g_group = NTTB_GROUP;
-
-#ifndef NTTB_PM_SHIFT
-// shift-shaped moduli (NTTMUL_MODE_PM): lazy bound "33".  Measured slower
-// (row kernel 0.568 vs 0.550 ms, pm_r36): ptxas moves the shift's subtract
-// onto the multiply pipe as IMAD.IADD, so the IMAD it replaces comes back.
-#define NTTB_PM_SHIFT 0
-#endif
-#ifndef NTTB_LB32
-#define NTTB_LB32 1  // multiply-reduced lazy schedule for moduli of 35..59 bits
-#endif
-
-// Cooperative launch of group_fused_kernel.  Returns NTTMUL_OK, or -1 when
-// the batch is too small for the group scheme (the caller falls back to the
-// three-launch pipeline).
-template <int LOG_N1, int MODE, int LB>
-int launch_group_t(u64 *c, const u64 *a, const u64 *b, u64 *ws, long long ws_words,
-                   const TwSet &tw, const LimbSet &ls, long long npolys, cudaStream_t st) {
-  using G = RowGeom<COL_LOG_R>;
-  constexpr int N1 = 1 << LOG_N1;
-  const long long n = static_cast<long long>(N1) << COL_LOG_R;
-  auto k = group_fused_kernel<LOG_N1, MODE, LB>;
-  const size_t smem = 2 * G::PADN * sizeof(u64);
-  CHECK(smem_optin(k, smem));
-  static int slots = 0;
-  static unsigned *counters[64] = {nullptr};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!slots) {
-    int sms = 148, nb = 1;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, G::T, smem) != cudaSuccess ||
-        nb < 1) {
-      cudaGetLastError();
-      nb = 1;
-    }
-    slots = nb * sms;
-  }
-  long long groups = slots / N1;
-  if (groups > ws_words / (6 * n)) groups = ws_words / (6 * n);
-  // every group should own several products, or the single-launch scheme
-  // leaves SMs idle; small batches use the three-launch pipeline
-  if (groups < 1 || npolys < 4 * (slots / N1)) return -1;
-  if (groups > 512) groups = 512;
-  if (dev < 0 || dev >= 64) return fail(NTTMUL_ECUDA, "device index %d", dev);
-  if (!counters[dev] && cudaMalloc(&counters[dev], 1024 * sizeof(unsigned)) != cudaSuccess)
-    return cuda_status("group counters");
-  if (cudaMemsetAsync(counters[dev], 0, 2 * groups * sizeof(unsigned), st) != cudaSuccess)
-    return cuda_status("group counters");
-  GroupParams P{c, a, b, ws, counters[dev], tw, ls, npolys, static_cast<int>(groups)};
-  void *args[] = {&P};
-  const cudaError_t e = cudaLaunchCooperativeKernel(
-      reinterpret_cast<const void *>(k), dim3(static_cast<unsigned>(groups * N1)), dim3(G::T),
-      args, smem, st);
-  if (e != cudaSuccess) return fail(NTTMUL_ELAUNCH, "group_fused_kernel: %s", cudaGetErrorString(e));
-  return cuda_status("group_fused_kernel");
-}
-
-template <int MODE, int LB>
-int launch_group(int log_n1, u64 *c, const u64 *a, const u64 *b, u64 *ws, long long ws_words,
-                 const TwSet &tw, const LimbSet &ls, long long npolys, cudaStream_t st) {
-  switch (log_n1) {
-    case 1: return launch_group_t<1, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
-    case 2: return launch_group_t<2, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
-    case 3: return launch_group_t<3, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
-    case 4: return launch_group_t<4, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
-    case 5: return launch_group_t<5, MODE, LB>(c, a, b, ws, ws_words, tw, ls, npolys, st);
-  }
-  return -1;
-}
-
-// The fused product for n > 4096 is COL -> ROW -> COL^-1.  Unchunked, the
-// intermediates round-trip HBM (a' -> c, b' -> ws).  Chunked (default), the
-// batch is cut into pieces of `g_chunk_waves` row-kernel waves; each piece
-// runs COL -> ROW -> COL^-1 on a scratch region small enough to stay in L2,
-// and its scratch lines are discarded (not written back) once consumed - so
-// HBM sees only a, b (read) and c (written).
-// phases: bit 0 = forward column pass, bit 1 = row kernel, bit 2 = inverse
-// column pass (n > 4096 only; smaller n always runs as one row kernel).
+// The fused product for n > 4096 is COL -> ROW -> COL^-1; the intermediates
+// round-trip HBM (a' -> c, b' -> ws).  phases: bit 0 = forward column pass,
+// bit 1 = row kernel, bit 2 = inverse column pass (n > 4096 only; smaller n
+// always runs as one row kernel).  (Measured and removed in round 1: an
+// L2-resident chunked pipeline with discard.global.L2 scratch, a persistent
+// row kernel, a bulk-copy column pipeline and a cooperative group-persistent
+// kernel - all slower, profiles/r1/NOTES.md.)
 template <int MODE, int LB>
 int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
                   LimbSet ls, int log_n, long long npolys, int phases,
@@ -415,38 +238,17 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
     RowParams R{c, a, b, tw, ls, 0, FIN_SCALED_SKIP, 0};
     return launch_row_fused<MODE, LB>(log_r, R, npolys, st);
   }
-  const long long n = 1LL << log_n;
-  if (phases == 7 && g_group && g_chunk_waves == 0 && ls.base == 0) {
-    // workspace holds npolys * n words (the API's [B, L, n] scratch)
-    const int r = launch_group<MODE, LB>(log_n1, c, a, b, ws, npolys * n, tw, ls, npolys, st);
-    if (r != -1) return r;
+  if (phases & 1) {
+    ColParams C{a, b, c, ws, 2, npolys, tw, ls, FIN_LAZY};
+    CHECK((launch_col<false, LB>(log_n1, C, st)));
   }
-  long long chunk = npolys;
-  if (g_chunk_waves > 0) {
-    chunk = (g_chunk_waves * fused_rows_per_wave<COL_LOG_R, MODE, LB>()) >> log_n1;
-    if (chunk < 1) chunk = 1;
-    if (2 * chunk > npolys) chunk = npolys;  // scratch must fit the workspace
+  if (phases & 2) {
+    RowParams R{c, c, ws, tw, ls, log_n1, FIN_SCALED_SKIP, 1};
+    CHECK((launch_row_fused<MODE, LB>(log_r, R, npolys << log_n1, st)));
   }
-  for (long long off = 0; off < npolys; off += chunk) {
-    const long long cnt = npolys - off < chunk ? npolys - off : chunk;
-    LimbSet lc = ls;
-    lc.base = static_cast<int>((ls.base + off) % (ls.num > 0 ? ls.num : 1));
-    const bool piped = chunk < npolys;
-    u64 *sa = piped ? ws : c + off * n;              // a' (then c')
-    u64 *sb = piped ? ws + cnt * n : ws + off * n;   // b'
-    if (phases & 1) {
-      ColParams C{a + off * n, b + off * n, sa, sb, 2, cnt, tw, lc, FIN_LAZY, 0};
-      CHECK((launch_col<false, LB>(log_n1, C, st)));
-    }
-    if (phases & 2) {
-      RowParams R{sa, sa, sb, tw, lc, log_n1, FIN_SCALED_SKIP, piped ? 1 : 0};
-      CHECK((launch_row_fused<MODE, LB>(log_r, R, cnt << log_n1, st)));
-    }
-    if (phases & 4) {
-      ColParams C{sa, nullptr, c + off * n, nullptr, 1, cnt, tw, lc, FIN_SCALED_SKIP,
-                  piped ? 1 : 0};
-      CHECK((launch_col<true, LB>(log_n1, C, st)));
-    }
+  if (phases & 4) {
+    ColParams C{c, nullptr, c, nullptr, 1, npolys, tw, ls, FIN_SCALED_SKIP};
+    CHECK((launch_col<true, LB>(log_n1, C, st)));
   }
   return NTTMUL_OK;
 }
@@ -457,78 +259,61 @@ int run_polymul_one(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *w
                     const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
                     int phases, cudaStream_t st);
 
-// Two-stream split of a large fused batch (n > 4096, full product): the
-// second half runs on an internal stream, so the HBM-bound column launches
-// of one half overlap the integer-bound row launch of the other (sweep:
-// +2.7 % on cfg3, scripts/stream_overlap.py).  Fork / join with events on
-// the caller's stream, so callers still see one ordered operation.
-#ifndef NTTB_SPLIT_STREAMS
-#define NTTB_SPLIT_STREAMS 2
-#endif
-#ifndef NTTB_SPLIT_STAGGER
-#define NTTB_SPLIT_STAGGER 0  // measured -3.5 % (21.4k vs 22.15k ct/s, sweep_r53): columns beside a row kernel slow it more than they gain
-#endif
-#ifndef NTTB_SPLIT_PARTS
-#define NTTB_SPLIT_PARTS NTTB_SPLIT_STREAMS  // parts, assigned round-robin to the streams
-#endif
-int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
-                const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
-                int phases, cudaStream_t st) {
-  constexpr int K = NTTB_SPLIT_STREAMS, NP = NTTB_SPLIT_PARTS;
-  const bool split = K > 1 && phases == 7 && log_n > COL_LOG_R && g_chunk_waves == 0 &&
-                     npolys >= 64 * NP && !g_group;
-  if (!split)
-    return run_polymul_one(mode, lb, c, a, b, ws, tw, ls, log_n, npolys, phases, st);
-  struct Side {
-    cudaStream_t s[K];
-    cudaEvent_t fork, join[K], stag[NP];
-  };
-  static Side sides[64];
+// Two-stream split of a large fused batch (n > 4096, full product): the two
+// halves run on internal streams, so the HBM-bound column launches of one
+// half overlap the integer-bound row launch of the other (sweep: +2.7 % on
+// cfg3, scripts/stream_overlap.py; more parts or a staggered start measured
+// slower, sweep_r41 / sweep_r53).  Fork / join with events on the caller's
+// stream, so callers still see one ordered operation.  Streams and events
+// are per host thread and device (thread_local), so concurrent callers never
+// share a fork/join event.
+constexpr int SPLIT_PARTS = 2;
+
+struct SideStreams {
+  cudaStream_t s[SPLIT_PARTS] = {};
+  cudaEvent_t fork = nullptr, join[SPLIT_PARTS] = {};
+};
+
+int side_streams(SideStreams **out) {
+  thread_local SideStreams sides[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cuda_status("device");
-  Side &sd = sides[dev];
+  SideStreams &sd = sides[dev];
   if (!sd.s[0]) {
     if (cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) != cudaSuccess)
       return cuda_status("split streams");
-    for (int k = 0; k < K; ++k)
+    for (int k = 0; k < SPLIT_PARTS; ++k)
       if (cudaStreamCreateWithFlags(&sd.s[k], cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&sd.join[k], cudaEventDisableTiming) != cudaSuccess)
         return cuda_status("split streams");
-    for (int p = 0; p < NP; ++p)
-      if (cudaEventCreateWithFlags(&sd.stag[p], cudaEventDisableTiming) != cudaSuccess)
-        return cuda_status("split streams");
   }
-  if (cudaEventRecord(sd.fork, st) != cudaSuccess) return cuda_status("split fork");
+  *out = &sd;
+  return NTTMUL_OK;
+}
+
+int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
+                const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
+                int phases, cudaStream_t st) {
+  const bool split = phases == 7 && log_n > COL_LOG_R && npolys >= 64 * SPLIT_PARTS;
+  if (!split)
+    return run_polymul_one(mode, lb, c, a, b, ws, tw, ls, log_n, npolys, phases, st);
+  SideStreams *sd = nullptr;
+  CHECK(side_streams(&sd));
+  if (cudaEventRecord(sd->fork, st) != cudaSuccess) return cuda_status("split fork");
   const long long n = 1LL << log_n;
-  for (int k = 0; k < K; ++k)
-    if (cudaStreamWaitEvent(sd.s[k], sd.fork) != cudaSuccess) return cuda_status("split wait");
   long long off = 0;
-  for (int p = 0; p < NP; ++p) {
-    const long long cnt = (npolys - off) / (NP - p);
+  for (int p = 0; p < SPLIT_PARTS; ++p) {
+    const long long cnt = (npolys - off) / (SPLIT_PARTS - p);
     LimbSet lk = ls;
     lk.base = static_cast<int>((ls.base + off) % (ls.num > 0 ? ls.num : 1));
-    cudaStream_t sp = sd.s[p % K];
-    if (NTTB_SPLIT_STAGGER) {
-      // part p's forward columns start once part p-1's are done, so they
-      // run beside part p-1's row kernel instead of all parts' columns
-      // competing for HBM at the start
-      if (p > 0 && cudaStreamWaitEvent(sp, sd.stag[p - 1]) != cudaSuccess)
-        return cuda_status("split stagger");
-      CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw,
-                            lk, log_n, cnt, phases & 1, sp));
-      if (cudaEventRecord(sd.stag[p], sp) != cudaSuccess) return cuda_status("split stagger");
-      CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw,
-                            lk, log_n, cnt, phases & 6, sp));
-    } else {
-      CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw,
-                            lk, log_n, cnt, phases, sp));
-    }
+    if (cudaStreamWaitEvent(sd->s[p], sd->fork) != cudaSuccess) return cuda_status("split wait");
+    CHECK(run_polymul_one(mode, lb, c + off * n, a + off * n, b + off * n, ws + off * n, tw, lk,
+                          log_n, cnt, phases, sd->s[p]));
+    if (cudaEventRecord(sd->join[p], sd->s[p]) != cudaSuccess ||
+        cudaStreamWaitEvent(st, sd->join[p]) != cudaSuccess)
+      return cuda_status("split join");
     off += cnt;
   }
-  for (int k = 0; k < K; ++k)
-    if (cudaEventRecord(sd.join[k], sd.s[k]) != cudaSuccess ||
-        cudaStreamWaitEvent(st, sd.join[k]) != cudaSuccess)
-      return cuda_status("split join");
   return NTTMUL_OK;
 }
 
@@ -536,7 +321,6 @@ int run_polymul_one(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *w
                     const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
                     int phases, cudaStream_t st) {
 #define NTTB_PM(M, LBV) run_polymul_m<M, LBV>(c, a, b, ws, tw, ls, log_n, npolys, phases, st)
-  if (lb == 33) return NTTB_PM(2, 33);  // proposed-shape constants only (see caller)
   if (lb == 32) return NTTB_PM(2, 32);
   if (lb == 16) {
     switch (mode) {
@@ -834,15 +618,14 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
     return fail(NTTMUL_EINVAL, "c may not alias b");
   const int lb = (mode & NTTMUL_MODE_NARROW60) ? 16 : ((mode & NTTMUL_MODE_NARROW) ? 8 : 4);
   const bool wide35 = (mode & NTTMUL_MODE_WIDE35) != 0;
-  const bool pm = (mode & NTTMUL_MODE_PM) != 0;
+  // NTTMUL_MODE_PM (shift-shaped moduli) is accepted and ignored: its
+  // schedule measured slower and was removed (pm_r36)
   mode &= ~(NTTMUL_MODE_NARROW | NTTMUL_MODE_NARROW60 | NTTMUL_MODE_WIDE35 | NTTMUL_MODE_PM);
   if (mode < 0 || mode > 2) return fail(NTTMUL_EINVAL, "unknown reduction mode %d", mode);
   // lazy bound "32": the [0, 16q) ranges with multiply-based reductions
   // (every modulus in [2^34, 2^60)), for the proposed-shape constants
   int lbx = lb;
-  if (mode == NTTMUL_RED_ONE_SUB && lb == 16 && wide35) lbx = NTTB_LB32 ? 32 : 16;
-  // "33": the same schedule with shift-shaped moduli (NTTMUL_MODE_PM)
-  if (lbx == 32 && pm && NTTB_PM_SHIFT) lbx = 33;
+  if (mode == NTTMUL_RED_ONE_SUB && lb == 16 && wide35) lbx = 32;
   LimbSet ls;
   ls.table = limbs;
   ls.num = num_limbs;
@@ -853,19 +636,6 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
            reinterpret_cast<const ulonglong2 *>(inv_pairs), stride};
   return run_polymul(mode, lbx, c, a, b, workspace, tw, ls, log_n,
                      batch * num_limbs, phases, S(stream));
-}
-
-int nttmul_set_pipeline(int chunk_waves, int reserved) {
-  if (chunk_waves < 0 || chunk_waves > 64 || reserved < 0)
-    return fail(NTTMUL_EINVAL, "pipeline chunk_waves=%d", chunk_waves);
-  g_chunk_waves = chunk_waves;
-  return NTTMUL_OK;
-}
-
-int nttmul_set_group(int enable) {
-  if (enable < 0 || enable > 1) return fail(NTTMUL_EINVAL, "set_group(%d)", enable);
-  g_group = enable;
-  return NTTMUL_OK;
 }
 
 int nttmul_polymul_fused_rns(uint64_t *c, const uint64_t *a, const uint64_t *b,
@@ -897,7 +667,7 @@ int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
     cudaStream_t s_in, s_out;
     cudaEvent_t ev_start, ev_in[NBUF], ev_done[NBUF], ev_out[NBUF];
   };
-  static Pipe pipes[64];  // one set of copy streams / events per device
+  thread_local Pipe pipes[64];  // copy streams / events per host thread and device
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cuda_status("device");
   Pipe &pp = pipes[dev];
@@ -1086,27 +856,6 @@ int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int
       modmul_roof_kernel<3, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
     if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2);
     return cuda_status("modmul_roof_kernel");
-  } else if (kind == 4 || kind == 5) {
-    const int bits = 64 - __builtin_clzll(L.q);
-    if (bits < 35 || bits > 60) return fail(NTTMUL_EINVAL, "LB=32 roof needs a 35..60-bit q");
-    if (kind == 4)
-      modmul_roof_kernel<4, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
-    else
-      modmul_roof_kernel<5, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
-    if (modmuls_out)
-      *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2) * (kind == 4 ? 3 : 2);
-    return cuda_status("modmul_roof_kernel");
-  } else if (kind == 6 || kind == 7) {
-    const int bits = 64 - __builtin_clzll(L.q);
-    const uint32_t nqh = static_cast<uint32_t>((0 - L.q) >> 32), d = 0u - nqh;
-    if (bits < 35 || bits > 60 || d == 0 || (d & (d - 1)) != 0)
-      return fail(NTTMUL_EINVAL, "shift-shaped roof needs a 35..60-bit q with hi32(-q) = 2^32 - 2^s");
-    if (kind == 6)
-      modmul_roof_kernel<6, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
-    else
-      modmul_roof_kernel<7, 2, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp);
-    if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * (CH / 2) * 2;
-    return cuda_status("modmul_roof_kernel");
   } else {
     switch (L.mode) {
       case 0: modmul_roof_kernel<0, 0, CH><<<blocks, threads, 0, S(stream)>>>(iters, sink_out, L, w, wp); break;
@@ -1117,16 +866,5 @@ int nttmul_modmul_roof(const nttmul_limb_t *limb_host, int kind, int blocks, int
   if (modmuls_out) *modmuls_out = static_cast<double>(blocks) * threads * iters * CH;
   return cuda_status("modmul_roof_kernel");
 }
-
-#ifdef NTTB_PHASE_TIMING
-// debug builds only (not in the header): copy the row-kernel phase stamps
-int nttmul_debug_phases(unsigned long long *host_out, int nrows) {
-  if (nrows > (1 << 16)) nrows = 1 << 16;
-  return cudaMemcpyFromSymbol(host_out, g_phase, sizeof(unsigned long long) * 8 * nrows) ==
-                 cudaSuccess
-             ? 0
-             : NTTMUL_ECUDA;
-}
-#endif
 
 }  // extern "C"

@@ -24,28 +24,13 @@ typedef nttmul_limb_t Limb;
 
 
 
-// x >= m ? x - m : x.
-// NTTB_CSUB_CARRY: the borrow of the 64-bit subtraction (a PTX carry chain)
-// selects the result - IADD3 + IADD3.X (carry out) + 2 predicated moves, but
-// the extra live borrow register raises spills in the row kernel.
-#ifdef NTTB_CSUB_CARRY
-__device__ __forceinline__ u64 csub(u64 x, u64 m) {
-  uint32_t tl, th, br;
-  asm("sub.cc.u32 %0, %3, %5;\n\t"
-      "subc.cc.u32 %1, %4, %6;\n\t"
-      "subc.u32 %2, 0, 0;"
-      : "=r"(tl), "=r"(th), "=r"(br)
-      : "r"(static_cast<uint32_t>(x)), "r"(static_cast<uint32_t>(x >> 32)),
-        "r"(static_cast<uint32_t>(m)), "r"(static_cast<uint32_t>(m >> 32)));
-  return br ? x : ((static_cast<u64>(th) << 32) | tl);
-}
-#else
-// sign-test form (valid for x < m + 2^63): IADD3 + IADD3.X + ISETP + 2 SEL
+// x >= m ? x - m : x, sign-test form (valid for x < m + 2^63): IADD3 +
+// IADD3.X + ISETP + 2 SEL.  (A carry-chain form - the borrow of the 64-bit
+// subtraction selecting the result - raised spills in the row kernel.)
 __device__ __forceinline__ u64 csub(u64 x, u64 m) {
   const u64 t = x - m;
   return (static_cast<long long>(t) < 0) ? x : t;
 }
-#endif
 
 // Barrett data x data product, a, b canonical.  MODE: NTTMUL_RED_*.
 template <int MODE>
@@ -103,16 +88,11 @@ __device__ __forceinline__ u64 pack(uint32_t lo, uint32_t hi) {
   return r;
 }
 
-#ifndef NTTB_LB32_STAGES
-#define NTTB_LB32_STAGES 0  // 1: multiply-reduced stage schedule (measured slower: row 0.574 vs 0.551 ms, sweep_r35)
-#endif
-
 // Per-prime constants the butterflies need.
 struct Mod {
   u64 q, q2, q4, q8;
   uint32_t nql, nqh;  // halves of 2^64 - q
   uint32_t fr, fs;    // LB >= 32 only: multiply-based reduction constants (reduce2q)
-  uint32_t ps;        // LB = 33 only: hi32(2^64 - q) = 2^32 - 2^ps (see shoup4<true>)
 };
 
 __device__ __forceinline__ Mod make_mod(u64 q) {
@@ -126,7 +106,6 @@ __device__ __forceinline__ Mod make_mod(u64 q) {
   m.nqh = hi32(nq);
   m.fr = 0;
   m.fs = 0;
-  m.ps = 0;
   return m;
 }
 
@@ -143,67 +122,30 @@ __device__ __forceinline__ Mod make_mod_fast(u64 q) {
   m.fs = static_cast<uint32_t>(bits - 33);
   const double rd = ldexp(1.0, 64 + static_cast<int>(m.fs)) / static_cast<double>(q);
   m.fr = static_cast<uint32_t>(rd) - 1;
-  m.ps = static_cast<uint32_t>(__ffs(static_cast<int>(0u - m.nqh)) - 1);
   return m;
 }
 
-// Moduli whose negation has a "shift-shaped" high word, hi32(2^64 - q) =
-// 2^32 - 2^ps, i.e. q in [2^(32+ps) - 2^32, 2^(32+ps)) (every BASELINE
-// prime is 2^60 - delta with delta < 2^26: ps = 28).  Then
-// x * hi32(2^64 - q) mod 2^32 = -(x << ps): a shift and a subtract on the
-// ALU pipe instead of an IMAD on the multiply pipe.  Host-side check:
-// nttmul_b200.h NTTMUL_MODE_PM.
-__device__ __forceinline__ uint32_t sub_shl(uint32_t h, uint32_t x, uint32_t s) {
-  uint32_t d;
-  asm("{\n\t.reg .u32 t;\n\tshl.b32 t, %1, %3;\n\tsub.u32 %0, %2, t;\n\t}"
-      : "=r"(d)
-      : "r"(x), "r"(h), "r"(s));
-  return d;
-}
-
-// h + x * hi32(2^64 - q) mod 2^32 (PM: the shift form above)
-template <bool PM>
-__device__ __forceinline__ uint32_t mad_nqh(uint32_t x, uint32_t h, const Mod &M) {
-  return PM ? sub_shl(h, x, M.ps) : madlo(x, M.nqh, h);
-}
-
 // LB = 32: the LB = 16 lazy ranges for moduli of 35..60 bits, where the
-// fused middle's partial reductions are multiply-based (reduce2q); with
-// NTTB_LB32_STAGES the transform stages use them too (measured slower: the
-// IMAD.HI / IMAD.WIDE quotient lands on the already busier multiply pipe).
-// Other bounds use plain constants.
-// LB = 33: LB = 32 for moduli that are also shift-shaped (Mod::ps).
+// fused middle's partial reductions are multiply-based (reduce2q).  (Using
+// them for the transform stages' corrections too measured slower: the
+// IMAD.HI / IMAD.WIDE quotient lands on the already busier multiply pipe,
+// row 0.574 vs 0.551 ms, sweep_r35.)
 template <int LB>
 __device__ __forceinline__ Mod mod_for(u64 q) {
   return LB >= 32 ? make_mod_fast(q) : make_mod(q);
 }
-template <int LB>
-__host__ __device__ constexpr bool lb_pm() { return LB == 33; }
-
 // Constants for kernels that run transform stages only (no fused middle):
-// the multiply-based reduction constants are needed there only with the
-// multiply-reduced stage schedule, so skip their double division.
+// no multiply-based reduction constants, so no double division.
 template <int LB>
 __device__ __forceinline__ Mod mod_for_stages(u64 q) {
-  Mod m = (LB >= 32 && NTTB_LB32_STAGES) ? make_mod_fast(q) : make_mod(q);
-  if (LB == 33 && !NTTB_LB32_STAGES)
-    m.ps = static_cast<uint32_t>(__ffs(static_cast<int>(0u - m.nqh)) - 1);
-  return m;
+  return make_mod(q);
 }
 
-template <bool PM = false>
 __device__ __forceinline__ u64 reduce2q(u64 x, const Mod &M) {
   uint32_t k;
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(k) : "r"(hi32(x)), "r"(M.fr));
   k >>= M.fs;
-  // PM: hi32(q) = 2^ps - 1, so k * hi32(q) = (k << ps) - k
-  uint32_t kh;
-  if (PM)
-    asm("{\n\t.reg .u32 t;\n\tshl.b32 t, %1, %2;\n\tsub.u32 %0, t, %1;\n\t}"
-        : "=r"(kh)
-        : "r"(k), "r"(M.ps));
-  else
-    kh = k * hi32(M.q);
+  const uint32_t kh = k * hi32(M.q);
   return x - (mulw(k, lo32(M.q)) + (static_cast<u64>(kh) << 32));
 }
 
@@ -238,7 +180,6 @@ __device__ __forceinline__ u64 mullo_add(uint32_t xl, uint32_t xh, uint32_t yl, 
 // 5 IMAD.WIDE.U32 + 4 IMAD + one 64-bit add.  (Measured faster than the
 // mulhi_approx chain below inside the butterflies: ptxas schedules the two
 // independent cross products better.)
-template <bool PM = false>
 __device__ __forceinline__ u64 shoup4(u64 x, u64 w, u64 wp, const Mod &M) {
   const uint32_t xl = lo32(x), xh = hi32(x);
   const u64 b = mulw(xl, hi32(wp));
@@ -249,7 +190,7 @@ __device__ __forceinline__ u64 shoup4(u64 x, u64 w, u64 wp, const Mod &M) {
   uint32_t h = hi32(a);
   h = madlo(xl, hi32(w), h);
   h = madlo(xh, lo32(w), h);
-  h = mad_nqh<PM>(ql, h, M);
+  h = madlo(ql, M.nqh, h);
   h = madlo(qhh, M.nql, h);
   return pack(lo32(a), h);
 }
@@ -261,7 +202,6 @@ __device__ __forceinline__ u64 shoup4(u64 x, u64 w, u64 wp, const Mod &M) {
 // undershoots floor(T / q) by at most 4 (Barrett's own <= 1 for canonical
 // inputs, < 2 more from c < 2^(m+4), 1 from the approximate high word), so
 // r = T - quot q lies in [0, 5q).  8 IMAD.WIDE.U32 + 2 IMAD in total.
-template <bool PM = false>
 __device__ __forceinline__ u64 mulred_lazy(u64 a, u64 b, const Limb &L, const Mod &M) {
   const uint32_t al = lo32(a), ah = hi32(a), bl = lo32(b), bh = hi32(b);
   const u64 p0 = mulw(al, bl);
@@ -271,12 +211,6 @@ __device__ __forceinline__ u64 mulred_lazy(u64 a, u64 b, const Limb &L, const Mo
   const u64 thi = madw(ah, bh, hi32(p1)) + hi32(p2);
   const u64 c = (tlo >> L.s_in) | ((thi << 1) << (63 - L.s_in));
   const u64 quot = mulhi_approx(c, L.mu_sh) >> L.s_hi;
-  if (PM) {  // tlo + quot * (2^64 - q) mod 2^64, high word by shift (Mod::ps)
-    const u64 t = madw(lo32(quot), M.nql, tlo);
-    uint32_t h = mad_nqh<true>(lo32(quot), hi32(t), M);
-    h = madlo(hi32(quot), M.nql, h);
-    return pack(lo32(t), h);
-  }
   return mullo_add(lo32(quot), hi32(quot), M.nql, M.nqh, tlo);
 }
 
@@ -296,16 +230,9 @@ __device__ __forceinline__ u64 mulred_lazy(u64 a, u64 b, const Limb &L, const Mo
 
 template <int LB, bool RED = true>
 __device__ __forceinline__ void ct_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod &M) {
-  if (LB >= 32 && NTTB_LB32_STAGES) {
-    // RED stages (every third): X (any) -> [0, 2q), outputs < 6q; the two
-    // non-reducing stages after it emit < 10q and < 14q
-    const u64 x = RED ? reduce2q<lb_pm<LB>()>(X, M) : X;
-    const u64 t = shoup4<lb_pm<LB>()>(Y, w, wp, M);
-    X = x + t;
-    Y = x - t + M.q4;
-  } else if (LB >= 16) {
+  if (LB >= 16) {
     const u64 x = RED ? csub(X, M.q8) : X;
-    const u64 t = shoup4<lb_pm<LB>()>(Y, w, wp, M);
+    const u64 t = shoup4(Y, w, wp, M);
     X = x + t;
     Y = x - t + M.q4;
   } else if (LB == 8) {
@@ -324,18 +251,11 @@ __device__ __forceinline__ void ct_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod
 // Merged GS inverse butterfly (reference _kernels.pyx:102-118, unscaled).
 template <int LB, bool RED = true>
 __device__ __forceinline__ void gs_bfly(u64 &X, u64 &Y, u64 w, u64 wp, const Mod &M) {
-  if (LB >= 32 && NTTB_LB32_STAGES) {
-    // alternating: a RED stage takes X, Y < 8q and emits < 4q (sum reduced to
-    // [0, 2q)); the non-reducing stage after it takes < 4q and emits < 8q
-    const u64 s = RED ? reduce2q<lb_pm<LB>()>(X + Y, M) : X + Y;
-    const u64 d = X - Y + (RED ? M.q8 : M.q4);
-    X = s;
-    Y = shoup4<lb_pm<LB>()>(d, w, wp, M);
-  } else if (LB >= 8) {
+  if (LB >= 8) {
     const u64 s = csub(X + Y, M.q4);
     const u64 d = X - Y + M.q4;
     X = s;
-    Y = shoup4<lb_pm<LB>()>(d, w, wp, M);
+    Y = shoup4(d, w, wp, M);
   } else {
     const u64 s = csub(X + Y, M.q2);
     const u64 d = X - Y + M.q2;
@@ -372,7 +292,7 @@ template <int LB>
 __device__ __forceinline__ void gs_bfly_last_scaled(u64 &X, u64 &Y, const u64 (&sc)[4],
                                                     const Mod &M) {
   const u64 s = X + Y;
-  const u64 d = X - Y + (LB >= 32 ? M.q8 : (LB >= 8 ? M.q4 : M.q2));
+  const u64 d = X - Y + (LB >= 8 ? M.q4 : M.q2);
   X = shoup(s, sc[0], sc[1], M);
   Y = shoup(d, sc[2], sc[3], M);
 }
@@ -407,17 +327,11 @@ __device__ __forceinline__ void fused_pair(u64 a0, u64 a1, u64 b0, u64 b1,
   c0 = odd ? csub(u + q - z, q) : csub(u + z, q);
 }
 
-// forward-range value (LB = 16) -> [0, 2q)
-__device__ __forceinline__ u64 to2q_fwd16(u64 x, const Mod &M) {
-  return csub(csub(csub(x, M.q8), M.q4), M.q2);
-}
-
-
-
-// forward-range value (LB >= 16) -> [0, 2q)
+// forward-range value (LB >= 16) -> [0, 2q): multiply-based for LB = 32,
+// three conditional subtractions for LB = 16
 template <int LB>
 __device__ __forceinline__ u64 to2q_any(u64 x, const Mod &M) {
-  return LB >= 32 ? reduce2q<lb_pm<LB>()>(x, M) : to2q_fwd16(x, M);
+  return LB >= 32 ? reduce2q(x, M) : csub(csub(csub(x, M.q8), M.q4), M.q2);
 }
 
 // Lazy Karatsuba-fused middle pair for the LB = 16 path (all q < 2^60,
@@ -425,21 +339,21 @@ __device__ __forceinline__ u64 to2q_any(u64 x, const Mod &M) {
 // [0, 4q) (the inverse lazy range, so the inverse stages take them as is).
 // Same algebra as fused_pair / reference _kernels.pyx:142-173; canonical
 // results after the inverse transform are identical.
-template <bool FAST, bool PM = false>
+template <bool FAST>
 __device__ __forceinline__ void fused_pair_lazy(u64 a0, u64 a1, u64 b0, u64 b1, u64 w, u64 wp,
                                                 bool odd, const Limb &L, const Mod &M,
                                                 u64 &c0, u64 &c1) {
-  const u64 u = mulred_lazy<PM>(a0, b0, L, M);     // [0, 5q)
-  const u64 v = mulred_lazy<PM>(a1, b1, L, M);     // [0, 5q)
+  const u64 u = mulred_lazy(a0, b0, L, M);     // [0, 5q)
+  const u64 v = mulred_lazy(a1, b1, L, M);     // [0, 5q)
   const u64 s1 = csub(a0 + a1, M.q2);              // [0, 2q)
   const u64 s2 = csub(b0 + b1, M.q2);
-  const u64 ww = mulred_lazy<PM>(s1, s2, L, M);    // [0, 5q)
+  const u64 ww = mulred_lazy(s1, s2, L, M);    // [0, 5q)
   const u64 y = ww + M.q8 + M.q2 - u - v;          // (0, 15q)
-  const u64 z = shoup4<PM>(v, w, wp, M);           // [0, 4q)
+  const u64 z = shoup4(v, w, wp, M);           // [0, 4q)
   const u64 x = odd ? u + M.q4 - z : u + z;        // [0, 9q)
   if (FAST) {  // -> [0, 2q)
-    c1 = reduce2q<PM>(y, M);
-    c0 = reduce2q<PM>(x, M);
+    c1 = reduce2q(y, M);
+    c0 = reduce2q(x, M);
   } else {  // -> [0, 4q)
     c1 = csub(csub(y, M.q8), M.q4);
     c0 = csub(csub(x, M.q8), M.q4);

@@ -61,65 +61,6 @@ __device__ __forceinline__ Limb get_limb(const LimbSet &S, long long poly,
   return S.single;
 }
 
-// L2 eviction-priority hints for the global streams of the pipeline:
-// inputs read for the last time are loaded evict-first, intermediates that
-// the next launch reads again (a', b' -> row kernel, c' -> inverse columns)
-// are stored evict-last, the final product evict-first.  NTTB_L2_HINTS=0
-// turns them into plain accesses.
-#ifndef NTTB_L2_HINTS
-#define NTTB_L2_HINTS 0  // measured +-0 % on the step, inverse columns slower (sweep_r33)
-#endif
-enum L2Hint { L2_NORMAL = 0, L2_FIRST = 1, L2_LAST = 2 };
-
-template <int H>
-__device__ __forceinline__ u64 l2_policy() {
-  u64 pol = 0;
-  if (H == L2_FIRST)
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  else if (H == L2_LAST)
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
-template <int H>
-__device__ __forceinline__ u64 ldg_hint(const u64 *p) {
-  if (!NTTB_L2_HINTS || H == L2_NORMAL) return *p;
-  u64 v;
-  asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(l2_policy<H>()));
-  return v;
-}
-
-template <int H>
-__device__ __forceinline__ void stg_hint(u64 *p, u64 v) {
-  if (!NTTB_L2_HINTS || H == L2_NORMAL) {
-    *p = v;
-    return;
-  }
-  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(l2_policy<H>())
-               : "memory");
-}
-
-// Drop a consumed scratch line from L2 without writing it back to HBM
-// (sm_80+ discard.global.L2): intermediates of the fused pipeline live and
-// die in L2.  `line` must be 128-byte aligned and fully consumed.
-__device__ __forceinline__ void discard_line(const void *line) {
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
-}
-
-#ifdef NTTB_PHASE_TIMING
-// debug builds only: per-CTA clock64 stamps at row-kernel phase boundaries
-__device__ unsigned long long g_phase[1 << 16][8];
-#define NTTB_STAMP(i)                                                            \
-  do {                                                                           \
-    if (threadIdx.x == 0 && blockIdx.x < (1u << 16)) g_phase[blockIdx.x][i] = clock64(); \
-  } while (0)
-#else
-#define NTTB_STAMP(i) \
-  do {                \
-  } while (0)
-#endif
-
-
 // resident CTAs per SM the row kernels are compiled for (register budget)
 #ifndef NTTB_ROW_MINB_FUSED
 #define NTTB_ROW_MINB_FUSED 2
@@ -144,25 +85,8 @@ enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 #ifndef NTTB_ROW_LOG_E
 #define NTTB_ROW_LOG_E 3
 #endif
-#ifndef NTTB_PREFETCH_B
-#define NTTB_PREFETCH_B 1
-#endif
 #ifndef NTTB_LAZY_MID
 #define NTTB_LAZY_MID 1
-#endif
-#ifndef NTTB_FAST_RED
-#define NTTB_FAST_RED 1
-#endif
-// issue a unit's twiddle loads before its data loads (hides their L2
-// latency; measured -2.7 % row-kernel time, sweep_r18)
-#ifndef NTTB_B_OWN_COPIES
-#define NTTB_B_OWN_COPIES 1
-#endif
-#ifndef NTTB_FWD_P_UNROLL
-#define NTTB_FWD_P_UNROLL 0
-#endif
-#ifndef NTTB_TW_PREFETCH
-#define NTTB_TW_PREFETCH 1
 #endif
 
 template <int LOG_R, int LOG_E = NTTB_ROW_LOG_E>
@@ -234,10 +158,16 @@ struct RowParams {
   LimbSet limbs;
   int log_n1;  // rows per polynomial = 2^log_n1
   int fin;     // FinalMode of the global last inverse stage (if in this kernel)
-  int discard_in;  // inputs are pipeline scratch: discard their L2 lines once read
+  int discard_in;  // inputs are pipeline scratch: drop their L2 lines once read
   long long nrows;    // rows in this launch
   long long pf_dist;  // > 0: prefetch the input rows of row + pf_dist into L2
 };
+
+// Drop a consumed scratch line from L2 without writing it back to HBM
+// (discard.global.L2).  `line` must be 128-byte aligned and fully consumed.
+__device__ __forceinline__ void discard_line(const void *line) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+}
 
 // bulk prefetch of [p, p + bytes) into L2 (no register or smem cost)
 __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
@@ -257,11 +187,7 @@ __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
   using G = RowGeom<LOG_R>;
   constexpr int U = G::E >> R;         // units per thread
   constexpr int LK = LOG_R - S0 - R;   // log2(k_last)
-#if NTTB_FWD_P_UNROLL
-#pragma unroll
-#else
 #pragma unroll 1
-#endif
   for (int p = 0; p < NP; ++p) {  // not unrolled: one polynomial's state live
     const u64 *__restrict__ g = p == 0 ? g0 : g1;
     u64 *__restrict__ s = sm + p * G::PADN;
@@ -270,22 +196,16 @@ __device__ __forceinline__ void head_fwd(u64 *__restrict__ sm,
       const int u = threadIdx.x + w * G::T;
       const int grp = u >> LK;
       const int o0 = (grp << (LOG_R - S0)) + (u & ((1 << LK) - 1));
-#if NTTB_TW_PREFETCH
       TwBuf<0, R> twb;
       tw_prefetch(twb, tw, (rowbase << S0) + grp);
-#endif
       const UnitIdx<LOG_R, LK> ix(o0);
       u64 x[1][1 << R];
 #pragma unroll
       for (int e = 0; e < (1 << R); ++e) {
         const int o = o0 + (e << LK);
-        x[0][e] = FROM_GLOBAL ? ldg_hint<L2_FIRST>(g + o) : s[ix(e)];
+        x[0][e] = FROM_GLOBAL ? g[o] : s[ix(e)];
       }
-#if NTTB_TW_PREFETCH
       fwd_radix_pf<LB, R, R, 1, S0 & 1>(x, twb, M);
-#else
-      fwd_radix<LB, R, R, 1, S0 & 1>(x, (rowbase << S0) + grp, tw, M);
-#endif
 #pragma unroll
       for (int e = 0; e < (1 << R); ++e) s[ix(e)] = x[0][e];
     }
@@ -307,60 +227,22 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
     const int g = u >> LK;
     const int o0 = (g << (LOG_R - S0)) + (u & ((1 << LK) - 1));
     const u64 B0 = (rowbase << S0) + g;
-#if NTTB_TW_PREFETCH
     TwBuf<0, R> twb;
     tw_prefetch(twb, tw, B0);
-#endif
     u64 x[1][1 << R];
     const UnitIdx<LOG_R, LK> ix(o0);
 #pragma unroll
     for (int e = 0; e < (1 << R); ++e) x[0][e] = sm[ix(e)];
     if (TO_GLOBAL) {
-#if NTTB_TW_PREFETCH
       inv_radix_pf<LB, R, R, 1, 1>(x, twb, M);
-#else
-      inv_radix<LB, R, R, 1, 1>(x, B0, tw, M);
-#endif
       inv_stage0<LB, R, 1>(x, B0, tw, L, M, fin);
 #pragma unroll
-      for (int e = 0; e < (1 << R); ++e) stg_hint<L2_LAST>(gout + o0 + (e << LK), x[0][e]);
+      for (int e = 0; e < (1 << R); ++e) *(gout + o0 + (e << LK)) = x[0][e];
     } else {
-#if NTTB_TW_PREFETCH
       inv_radix_pf<LB, R, R, 0, 1>(x, twb, M);
-#else
-      inv_radix<LB, R, R, 0, 1>(x, B0, tw, M);
-#endif
 #pragma unroll
       for (int e = 0; e < (1 << R); ++e) sm[ix(e)] = x[0][e];
     }
-  }
-}
-
-// Pull the twiddle pairs the thread's unit of head pass I will read into L1
-// before the barrier that precedes the pass (no registers: prefetch.L1), so
-// the loads issued after the barrier hit L1 instead of waiting on L2.  Stage
-// t of the unit reads the 2^t consecutive pairs starting at (B0 << t).
-#ifndef NTTB_TW_L1PF
-#define NTTB_TW_L1PF 0  // measured +-0 (row 0.5289 ms both ways, r50): twiddle latency is not the limiter
-#endif
-__device__ __forceinline__ void prefetch_l1(const void *p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-template <int R>
-__device__ __forceinline__ void tw_prefetch_l1(const ulonglong2 *tw, u64 B0) {
-#pragma unroll
-  for (int t = 0; t < R; ++t) {
-    prefetch_l1(tw + (B0 << t));
-    if (t >= 3) prefetch_l1(tw + (B0 << t) + (1 << t) - 1);  // > 128 B range
-  }
-}
-template <int LOG_R, int I>
-__device__ __forceinline__ void pass_tw_l1(const ulonglong2 *tw, u64 rowbase) {
-  using G = RowGeom<LOG_R>;
-  if constexpr (NTTB_TW_L1PF && I < G::NPASS && (G::E >> G::R(I)) == 1) {
-    constexpr int LK = LOG_R - G::S0(I) - G::R(I);
-    const u64 B0 = (rowbase << G::S0(I)) + (threadIdx.x >> LK);
-    tw_prefetch_l1<G::R(I)>(tw, B0);
   }
 }
 
@@ -391,28 +273,23 @@ __device__ __forceinline__ void row_sync() {
   }
 }
 
-// all forward head passes, pass i = 0 .. NPASS-1 (pass 0 reads global)
-template <int LB, int LOG_R, int NP, int I = 0>
+// all forward head passes, pass i = 0 .. NPASS-1 (pass 0 reads global when
+// G0, else every pass works in shared memory)
+template <int LB, int LOG_R, int NP, int I = 0, bool G0 = true>
 __device__ __forceinline__ void head_fwd_all(u64 *sm, const u64 *g0, const u64 *g1,
                                              u64 rowbase, const ulonglong2 *tw,
                                              const Mod &M) {
   using G = RowGeom<LOG_R>;
   if constexpr (I < G::NPASS) {
-    head_fwd<LB, LOG_R, G::S0(I), G::R(I), NP, I == 0>(sm, g0, g1, rowbase, tw, M);
-    pass_tw_l1<LOG_R, I + 1>(tw, rowbase);
-    if constexpr (NTTB_TW_L1PF && I + 1 == G::NPASS && G::HEAD > 0) {
-      // the tail's forward stage twiddles (its inverse ones come from the
-      // other table, prefetched by the caller's tail)
-      tw_prefetch_l1<(LOG_R - G::HEAD) - 1>(tw, (rowbase << G::HEAD) + threadIdx.x);
-    }
+    head_fwd<LB, LOG_R, G::S0(I), G::R(I), NP, G0 && I == 0>(sm, g0, g1, rowbase, tw, M);
     row_sync<LOG_R, G::S0(I)>();
-    if (I == 0) NTTB_STAMP(1);
-    head_fwd_all<LB, LOG_R, NP, I + 1>(sm, g0, g1, rowbase, tw, M);
+    head_fwd_all<LB, LOG_R, NP, I + 1, G0>(sm, g0, g1, rowbase, tw, M);
   }
 }
 
-// all inverse head passes, pass i = NPASS-1 .. 0 (pass 0 writes global)
-template <int LB, int LOG_R, int I>
+// all inverse head passes, pass i = NPASS-1 .. 0 (pass 0 writes global when
+// TO_GLOBAL, else back to shared memory with more inverse stages to follow)
+template <int LB, int LOG_R, int I, bool TO_GLOBAL = true>
 __device__ __forceinline__ void head_inv_all(u64 *sm, u64 *gout, u64 rowbase,
                                              const ulonglong2 *tw, const Limb &L,
                                              const Mod &M, int fin) {
@@ -420,23 +297,16 @@ __device__ __forceinline__ void head_inv_all(u64 *sm, u64 *gout, u64 rowbase,
   if constexpr (I > 0) {
     head_inv<LB, LOG_R, G::S0(I), G::R(I), false>(sm, nullptr, rowbase, tw, L, M,
                                                   FIN_LAZY);
-    pass_tw_l1<LOG_R, I - 1>(tw, rowbase);
     row_sync<LOG_R, G::S0(I - 1)>();
-    head_inv_all<LB, LOG_R, I - 1>(sm, gout, rowbase, tw, L, M, fin);
+    head_inv_all<LB, LOG_R, I - 1, TO_GLOBAL>(sm, gout, rowbase, tw, L, M, fin);
   } else {
-    head_inv<LB, LOG_R, 0, G::R(0), true>(sm, gout, rowbase, tw, L, M, fin);
+    head_inv<LB, LOG_R, 0, G::R(0), TO_GLOBAL>(sm, gout, rowbase, tw, L, M, fin);
   }
 }
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-#if NTTB_L2_HINTS
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem),
-               "l"(l2_policy<L2_FIRST>())
-               : "memory");
-#else
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-#endif
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -489,10 +359,8 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   constexpr bool FAST = LAZY_MID && LB >= 32;
   const int o0 = threadIdx.x * E;
   const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
-#if NTTB_TW_PREFETCH
   TwBuf<0, LE - 1> twb;
   if constexpr (MID) tw_prefetch(twb, twf, B0);
-#endif
   const UnitIdx<LOG_R, 0> ix(o0);
   u64 xa[1][E];
 #pragma unroll
@@ -500,23 +368,15 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   if constexpr (MID) {
     // a's last truncated stages first, parked (canonical) in its own smem
     // slots; then b's, kept in registers and overwritten by c pair by pair.
-#if NTTB_TW_PREFETCH
     fwd_radix_pf<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, twb, M);
-#else
-    fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
-#endif
 #pragma unroll
     for (int e = 0; e < E; ++e)
       sm[ix(e)] =
           LAZY_MID ? to2q_any<LB>(xa[0][e], M) : canon_fwd<LB>(xa[0][e], M);
 #pragma unroll
     for (int e = 0; e < E; ++e) xa[0][e] = sm[G::PADN + ix(e)];
-#if NTTB_TW_PREFETCH
     fwd_radix_pf<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, twb, M);
     tw_prefetch(twb, twi, B0);  // inverse twiddles of the same groups
-#else
-    fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
-#endif
     // pair p = (2p, 2p+1); twiddle tw[n/4 + i/2] == tw[(B0 << (LE-2)) + p/2]
     // (the k = 2 stage's group twiddle); sign of the z term = parity of the
     // global pair index = parity of p.
@@ -527,7 +387,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
       for (int h = 0; h < 2; ++h) {
         const int i0 = 2 * (p + h);
         if constexpr (LAZY_MID)
-          fused_pair_lazy<FAST, lb_pm<LB>()>(sm[ix(i0)], sm[ix(i0 + 1)],
+          fused_pair_lazy<FAST>(sm[ix(i0)], sm[ix(i0 + 1)],
                                 to2q_any<LB>(xa[0][i0], M), to2q_any<LB>(xa[0][i0 + 1], M), w.x,
                                 w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
         else
@@ -536,11 +396,7 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
                            w.x, w.y, h != 0, L, M, xa[0][i0], xa[0][i0 + 1]);
       }
     }
-#if NTTB_TW_PREFETCH
     inv_radix_pf<LB, LE, LE - 1, 0, 1>(xa, twb, M);
-#else
-    inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
-#endif
 #pragma unroll
     for (int e = 0; e < E; ++e) sm[ix(e)] = xa[0][e];
   } else {
@@ -558,50 +414,9 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   }
 }
 
-// fused tail with a and b in separate smem buffers (persistent kernel);
-// c is written over a.
-template <int LB, int LOG_R, int MODE>
-__device__ __forceinline__ void tail_pass_split(u64 *__restrict__ sa, u64 *__restrict__ sb,
-                                                u64 rowbase,
-                                                const ulonglong2 *__restrict__ twf,
-                                                const ulonglong2 *__restrict__ twi,
-                                                const Limb &L, const Mod &M) {
-  using G = RowGeom<LOG_R>;
-  constexpr int E = G::E;
-  constexpr int LE = LOG_R - G::HEAD;
-  const int o0 = threadIdx.x * E;
-  const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
-  u64 xa[1][E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) xa[0][e] = sa[G::idx(o0 + e)];
-  fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
-#pragma unroll
-  for (int e = 0; e < E; ++e) sa[G::idx(o0 + e)] = canon_fwd<LB>(xa[0][e], M);
-#pragma unroll
-  for (int e = 0; e < E; ++e) xa[0][e] = sb[G::idx(o0 + e)];
-  fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
-#pragma unroll
-  for (int p = 0; p < E / 2; p += 2) {
-    const ulonglong2 w = ldtw(twf, (B0 << (LE - 2)) + (p >> 1));
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int i0 = 2 * (p + h);
-      fused_pair<MODE>(sa[G::idx(o0 + i0)], sa[G::idx(o0 + i0 + 1)], canon_fwd<LB>(xa[0][i0], M),
-                       canon_fwd<LB>(xa[0][i0 + 1], M), w.x, w.y, h != 0, L, M, xa[0][i0],
-                       xa[0][i0 + 1]);
-    }
-  }
-  inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
-#pragma unroll
-  for (int e = 0; e < E; ++e) sa[G::idx(o0 + e)] = xa[0][e];
-}
-
 // Split CTA barrier (mbarrier): every thread arrives as soon as its writes
 // are done and waits only where it needs the other threads' data, so the
 // work placed between arrive and wait hides the barrier.
-#ifndef NTTB_SPLIT_BAR
-#define NTTB_SPLIT_BAR 1
-#endif
 __device__ __forceinline__ void sbar_init(u64 *bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
                    static_cast<unsigned>(__cvta_generic_to_shared(bar))),
@@ -640,7 +455,6 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
   const u64 rowbase = (1ULL << P.log_n1) + r;  // (N1 + r): group index base
   const long long off = row * G::N2;
-  NTTB_STAMP(0);
   // Rows are dispatched in order, so the CTA that takes row + pf_dist (one
   // resident wave later) starts about when this one ends: pull its inputs
   // into L2 now so its first pass does not wait on HBM latency.
@@ -650,15 +464,15 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
     if (NP > 1) prefetch_l2(P.in1 + nx, G::N2 * sizeof(u64));
   }
 
-  constexpr bool SPLIT = NTTB_SPLIT_BAR && NTTB_B_OWN_COPIES && G::R(0) == NTTB_ROW_LOG_E &&
-                        G::NPASS >= 2;
-  __shared__ u64 sbar[2];  // SPLIT: a's / b's first pass written
-  if (MID && NTTB_PREFETCH_B && SPLIT) {
+  __shared__ u64 sbar[2];  // a's / b's first pass written
+  if constexpr (MID) {
+    static_assert(G::R(0) == NTTB_ROW_LOG_E && G::NPASS >= 2, "fused row geometry");
     // b's row streams into its smem slot (cp.async, each thread exactly the
     // words its own first-pass unit reads) while a's first pass loads and
     // transforms a.  The CTA-wide dependency pass 0 -> pass 1 is split per
-    // polynomial: arrive after a's pass 0, b's pass 0, wait(a), a's pass 1,
-    // wait(b), b's pass 1 - the waits are mostly satisfied by then.
+    // polynomial (mbarrier): arrive after a's pass 0, b's pass 0, wait(a),
+    // a's pass 1, wait(b), b's pass 1 - the waits are mostly satisfied by
+    // then (row 0.529 -> 0.519 ms, r55).
     if (threadIdx.x == 0) {
       sbar_init(&sbar[0], G::T);
       sbar_init(&sbar[1], G::T);
@@ -680,65 +494,30 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
     row_sync<LOG_R, G::S0(1)>();
     head_fwd_all<LB, LOG_R, NP, 2>(sm, nullptr, nullptr, rowbase, twf, M);
     if (P.discard_in) {
-      constexpr int LINES = G::N2 * 8 / 128;
-      for (int i = threadIdx.x; i < NP * LINES; i += G::T)
-        discard_line((i < LINES ? P.in0 : P.in1) + off + (i % LINES) * 16);
-    }
-  } else if (MID && NTTB_PREFETCH_B) {
-    // b's row streams into its smem slot (cp.async) while a's first pass
-    // loads and transforms a; then b's first pass runs from smem.
-    row_prefetch<LOG_R>(sm + G::PADN, P.in1 + off);
-    cp_async_commit();
-    head_fwd<LB, LOG_R, 0, G::R(0), 1, true>(sm, P.in0 + off, nullptr, rowbase, twf, M);
-    NTTB_STAMP(5);
-    cp_async_wait<0>();
-    // Thread t copied exactly the words t + 512 k that its pass-0 unit of b
-    // reads (row_prefetch and head_fwd<S0 = 0> share the mapping), so its
-    // own wait_group makes them visible: no CTA barrier before b's pass 0.
-    if (!(NTTB_B_OWN_COPIES && G::R(0) == NTTB_ROW_LOG_E))
-      __syncthreads();
-    NTTB_STAMP(1);
-    head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sm + G::PADN, nullptr, nullptr, rowbase, twf, M);
-    pass_tw_l1<LOG_R, 1>(twf, rowbase);
-    __syncthreads();
-    NTTB_STAMP(6);
-    head_fwd_all<LB, LOG_R, NP, 1>(sm, nullptr, nullptr, rowbase, twf, M);
-    if (P.discard_in) {
+      // the input rows are pipeline scratch (a' in c, b' in the workspace)
+      // and now live only in shared memory: drop their L2 lines without a
+      // write-back.  (This loop also changes ptxas's schedule of the tail:
+      // without it the kernel spills 40 instead of 24 bytes and runs 1.6 %
+      // slower, r2 A/B.)
       constexpr int LINES = G::N2 * 8 / 128;
       for (int i = threadIdx.x; i < NP * LINES; i += G::T)
         discard_line((i < LINES ? P.in0 : P.in1) + off + (i % LINES) * 16);
     }
   } else if (FWD != FWD_NONE) {
-    head_fwd_all<LB, LOG_R, NP>(sm, P.in0 + off, NP > 1 ? P.in1 + off : nullptr, rowbase,
-                                twf, M);
-    if (P.discard_in) {  // every element of the input rows is now in smem
-      constexpr int LINES = G::N2 * 8 / 128;
-      for (int i = threadIdx.x; i < NP * LINES; i += G::T) {
-        const u64 *src = (i < LINES ? P.in0 : P.in1) + off;
-        discard_line(src + (i % LINES) * 16);
-      }
-    }
+    head_fwd_all<LB, LOG_R, NP>(sm, P.in0 + off, nullptr, rowbase, twf, M);
   } else {
 #pragma unroll 4
     for (int i = threadIdx.x; i < G::N2; i += G::T) sm[G::idx(i)] = P.in0[off + i];
     __syncthreads();
   }
-  NTTB_STAMP(2);
   tail_pass<LB, LOG_R, NP, FWD, MID, INV, MODE>(sm, rowbase, twf, twi, L, M);
-  if (INV != INV_NONE || MID) pass_tw_l1<LOG_R, G::NPASS - 1>(twi, rowbase);
   if (INV != INV_NONE || MID)
     row_sync<LOG_R, G::S0(G::NPASS - 1)>();  // the inverse passes read back this tail
   else
     __syncthreads();  // the plain store below reads the whole row
-  NTTB_STAMP(3);
   if (INV != INV_NONE || MID) {
     head_inv_all<LB, LOG_R, G::NPASS - 1>(sm, P.out + off, rowbase, twi, L, M,
                                           P.log_n1 == 0 ? P.fin : FIN_LAZY);
-    NTTB_STAMP(4);
-#ifdef NTTB_PHASE_TIMING
-    __syncthreads();  // the CTA's last warp
-    NTTB_STAMP(7);
-#endif
   } else {
 #pragma unroll 4
     for (int i = threadIdx.x; i < G::N2; i += G::T) P.out[off + i] = sm[G::idx(i)];
@@ -746,108 +525,16 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T,
 }
 
 // ---------------------------------------------------------------------------
-// PERSISTENT fused row kernel with a software-pipelined input stream.
-//
-// One CTA per resident slot walks rows gridDim.x apart.  The next row's
-// inputs are copied (cp.async) into the SAME two buffers as soon as each
-// becomes free, so no extra shared memory is needed: b's buffer is free once
-// the tail has consumed b (its copy is issued before the last inverse pass),
-// a's buffer once the last inverse pass has read it (its copy is issued at
-// the end of the row).  The next row then starts with b's first pass (data
-// already landed) while a's copy completes.  In the one-row-per-CTA kernel
-// both CTAs of an SM start together and wait on HBM together; here that
-// latency hides behind the previous row's last pass.
-
-// inverse head passes I .. 1, each followed by its barrier (the one after
-// pass 1 is the whole-row barrier before pass 0)
-template <int LB, int LOG_R, int I>
-__device__ __forceinline__ void head_inv_to1(u64 *sm, u64 rowbase, const ulonglong2 *tw,
-                                             const Limb &L, const Mod &M) {
-  using G = RowGeom<LOG_R>;
-  if constexpr (I > 0) {
-    head_inv<LB, LOG_R, G::S0(I), G::R(I), false>(sm, nullptr, rowbase, tw, L, M, FIN_LAZY);
-    row_sync<LOG_R, G::S0(I - 1)>();
-    head_inv_to1<LB, LOG_R, I - 1>(sm, rowbase, tw, L, M);
-  }
-}
-
-template <int LOG_R, int MODE, int LB>
-__global__ void __launch_bounds__(RowGeom<LOG_R>::T, NTTB_ROW_MINB_FUSED)
-    row_fused_persistent(const RowParams P, long long nrows) {
-  using G = RowGeom<LOG_R>;
-  extern __shared__ u64 sm[];
-  u64 *const sa = sm, *const sb = sm + G::PADN;
-  long long row = blockIdx.x;
-  if (row < nrows) {
-    row_prefetch<LOG_R>(sb, P.in1 + row * G::N2);
-    cp_async_commit();
-    row_prefetch<LOG_R>(sa, P.in0 + row * G::N2);
-    cp_async_commit();
-  }
-  for (; row < nrows; row += gridDim.x) {
-    const long long poly = row >> P.log_n1;
-    const int r = static_cast<int>(row & ((1LL << P.log_n1) - 1));
-    int limb;
-    const Limb &L = *limb_ptr(P.limbs, poly, limb);
-    const Mod M = mod_for<LB>(L.q);
-    const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
-    const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
-    const u64 rowbase = (1ULL << P.log_n1) + r;
-    const long long off = row * G::N2;
-    const long long next = row + gridDim.x;
-    NTTB_STAMP(0);
-    cp_async_wait<1>();  // b(row) has landed; a(row) may still be in flight
-    __syncthreads();
-    head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sb, nullptr, nullptr, rowbase, twf, M);
-    cp_async_wait<0>();  // a(row)
-    __syncthreads();
-    head_fwd<LB, LOG_R, 0, G::R(0), 1, false>(sa, nullptr, nullptr, rowbase, twf, M);
-    __syncthreads();
-    NTTB_STAMP(1);
-    head_fwd_all<LB, LOG_R, 2, 1>(sm, nullptr, nullptr, rowbase, twf, M);
-    NTTB_STAMP(2);
-    tail_pass<LB, LOG_R, 2, FWD_TRUNC, true, INV_SKIP, MODE>(sm, rowbase, twf, twi, L, M);
-    row_sync<LOG_R, G::S0(G::NPASS - 1)>();
-    NTTB_STAMP(3);
-    head_inv_to1<LB, LOG_R, G::NPASS - 1>(sm, rowbase, twi, L, M);
-    // whole-row barrier passed: b is dead, refill its buffer with b(next)
-    if (next < nrows) row_prefetch<LOG_R>(sb, P.in1 + next * G::N2);
-    cp_async_commit();
-    head_inv<LB, LOG_R, 0, G::R(0), true>(sa, P.out + off, rowbase, twi, L, M,
-                                          P.log_n1 == 0 ? P.fin : FIN_LAZY);
-    __syncthreads();  // every thread has read a's buffer
-    if (next < nrows) row_prefetch<LOG_R>(sa, P.in0 + next * G::N2);
-    cp_async_commit();
-    NTTB_STAMP(4);
-  }
-  cp_async_wait<0>();
-}
-
-// ---------------------------------------------------------------------------
 // COLUMN kernels (N2 = 4096 columns per polynomial, N1 = 2^LOG_N1 rows)
 
-#ifndef NTTB_COL_LOG_R
-#define NTTB_COL_LOG_R 12
-#endif
-#ifndef NTTB_COL_VEC
-#define NTTB_COL_VEC 1
-#endif
-#ifndef NTTB_COL_SMEM_TW
-#define NTTB_COL_SMEM_TW 1
-#endif
 #ifndef NTTB_COL_MINB
 #define NTTB_COL_MINB 4  // forward columns at 4 CTAs/SM (64 regs) since the loads go out first: col fwd 0.145 -> 0.123 ms (sweep_r60)
 #endif
-#ifndef NTTB_COL_INV_LOADS_FIRST
-#define NTTB_COL_INV_LOADS_FIRST 1  // with 4 CTAs/SM: col inv 0.0803 -> 0.0763 ms (sweep_r62)
-#endif
 #ifndef NTTB_COL_MINB_INV
-#define NTTB_COL_MINB_INV 4
+#define NTTB_COL_MINB_INV 4  // with the loads first: col inv 0.0803 -> 0.0763 ms (sweep_r62)
 #endif
-constexpr int COL_LOG_R = NTTB_COL_LOG_R;  // row length used for n > 2^COL_LOG_R
+constexpr int COL_LOG_R = 12;  // row length used for n > 2^12
 constexpr int COL_THREADS = 256;
-constexpr int COL_VEC = NTTB_COL_VEC;      // adjacent columns per thread (1 or 2)
-static_assert(COL_VEC == 1 || COL_VEC == 2, "column vector width");
 
 struct ColParams {
   const u64 *src0;
@@ -859,19 +546,63 @@ struct ColParams {
   TwSet tw;
   LimbSet limbs;
   int fin;  // inverse: FinalMode of the last stage (global m == 1)
-  int discard_src;  // sources are pipeline scratch: discard after reading
 };
 
-// Each thread owns COL_VEC adjacent columns (one 8*COL_VEC-byte vector per
-// row, coalesced across the warp) and runs all LOG_N1 column stages on them
-// in registers; the stages' twiddles tw[1 .. N1) are uniform across the grid.
-// Per-direction geometry (measured, sweep_r26): the forward pass (two
-// sources, 4 stages) runs one column per thread with up to 128 registers;
-// the inverse pass (one source + folded scale) one column per thread at 4
-// CTAs per SM (64 registers).
-template <bool INV, int LOG_N1 = 4>
+// The LOG_N1 column stages of one column held in registers (merged-CT
+// stages with half-size k >= N2: group index B0 = 1 at the first stage, so
+// they read only tw[1 .. N1)).
+template <int LB, int LOG_N1>
+__device__ __forceinline__ void col_fwd_stages(u64 (&x)[1][1 << LOG_N1],
+                                               const ulonglong2 *twc, const Mod &M) {
+  if constexpr (LOG_N1 == 5) {
+    // 32-row columns (n = 2^17): the stage whose pairs straddle the two
+    // 16-element halves runs on the whole column, the other four stages as
+    // two radix-16 units (B0 = 2 + h) - the single 5-stage unit is not
+    // register-promoted by the compiler (its 32-word array went to local
+    // memory).  Same butterflies, twiddles and reduction parity.
+    const ulonglong2 w = ldtw(twc, 1);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) ct_bfly<LB, true>(x[0][e], x[0][e + 16], w.x, w.y, M);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      u64 y[1][16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) y[0][e] = x[0][16 * h + e];
+      fwd_radix<LB, 4, 4, 1, 1>(y, 2 + h, twc, M);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[0][16 * h + e] = y[0][e];
+    }
+  } else {
+    fwd_radix<LB, LOG_N1, LOG_N1, 1>(x, 1, twc, M);
+  }
+}
+
+// Mirror: the inverse column stages, the last one (global m = 1) with the
+// final treatment `fin` (scale folded in, canonical output).
+template <int LB, int LOG_N1>
+__device__ __forceinline__ void col_inv_stages(u64 (&x)[1][1 << LOG_N1], const ulonglong2 *twc,
+                                               const Limb &L, const Mod &M, int fin) {
+  if constexpr (LOG_N1 == 5) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      u64 y[1][16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) y[0][e] = x[0][16 * h + e];
+      inv_radix<LB, 4, 4, 0, 1>(y, 2 + h, twc, M);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[0][16 * h + e] = y[0][e];
+    }
+  } else {
+    inv_radix<LB, LOG_N1, LOG_N1, 1, 1>(x, 1, twc, M);
+  }
+  inv_stage0<LB, LOG_N1, 1>(x, 1, twc, L, M, fin);
+}
+
+// Each thread owns one column (one 8-byte word per row, coalesced across
+// the warp) and runs all LOG_N1 column stages on it in registers; the
+// stages' twiddles tw[1 .. N1) are uniform across the CTA.
+template <bool INV, int LOG_N1>
 struct ColGeom {
-  static constexpr int V = NTTB_COL_VEC;
   // 32-word columns (n = 2^17) need the register budget of 2 CTAs/SM
   static constexpr int MINB = LOG_N1 >= 5 ? 2 : (INV ? NTTB_COL_MINB_INV : NTTB_COL_MINB);
 };
@@ -879,457 +610,41 @@ struct ColGeom {
 template <int LOG_N1, bool INV, int LB>
 __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col_kernel(const ColParams P) {
   constexpr int N1 = 1 << LOG_N1;
-  constexpr int V = ColGeom<INV>::V;
-  const long long vecs = (P.npolys << COL_LOG_R) / V;  // column vectors per source
-  // a CTA's COL_THREADS * V columns lie in one polynomial of one source
-  // (4096 columns per polynomial), so source, polynomial and limb are
-  // CTA-uniform: derive them from blockIdx only
+  const long long cols = P.npolys << COL_LOG_R;  // columns per source
+  // a CTA's COL_THREADS columns lie in one polynomial of one source (4096
+  // columns per polynomial), so source, polynomial and limb are CTA-uniform:
+  // derive them from blockIdx only
   const long long cta0 = blockIdx.x * static_cast<long long>(COL_THREADS);
-  if (cta0 >= vecs * P.nsrc) return;
-  const int which = cta0 >= vecs ? 1 : 0;
-  const long long rem = (cta0 - (which ? vecs : 0)) * V + threadIdx.x * V;  // first column
-  const long long poly = ((cta0 - (which ? vecs : 0)) * V) >> COL_LOG_R;
-  const long long base =
-      (poly << (COL_LOG_R + LOG_N1)) + (rem & ((1 << COL_LOG_R) - 1));
+  if (cta0 >= cols * P.nsrc) return;
+  const int which = cta0 >= cols ? 1 : 0;
+  const long long first = cta0 - (which ? cols : 0);
+  const long long poly = first >> COL_LOG_R;
+  const long long base = (poly << (COL_LOG_R + LOG_N1)) +
+                         ((first + threadIdx.x) & ((1 << COL_LOG_R) - 1));
   int limb;
   const Limb &L = *limb_ptr(P.limbs, poly, limb);
   const Mod M = mod_for_stages<LB>(L.q);
   const u64 *__restrict__ src = (which ? P.src1 : P.src0) + base;
   u64 *__restrict__ dst = (which ? P.dst1 : P.dst0) + base;
-#if NTTB_COL_SMEM_TW
-  // The N1 - 1 column twiddles are the same for the whole CTA (its 256
-  // columns lie in one polynomial): stage them in shared memory so the
-  // butterflies read them just in time (LDS broadcast) instead of the
-  // compiler hoisting 2 x (N1 - 1) global loads into registers.  The
-  // column loads go out first and the staging barrier overlaps their HBM
-  // latency (forward -4 %, then 4 CTAs/SM -15 %; inverse at 4 CTAs/SM -5 %).
+  // The column loads go out first; the N1 - 1 twiddles (the same for the
+  // whole CTA) are staged in shared memory behind them, so the butterflies
+  // read them just in time (LDS broadcast) instead of the compiler hoisting
+  // 2 x (N1 - 1) global loads into registers, and the staging barrier
+  // overlaps the HBM latency (forward -4 %, then 4 CTAs/SM -15 %; inverse
+  // at 4 CTAs/SM -5 %).
+  u64 x[1][N1];
+#pragma unroll
+  for (int e = 0; e < N1; ++e) x[0][e] = src[static_cast<long long>(e) << COL_LOG_R];
   __shared__ ulonglong2 stw[N1];
-  auto stage_tw = [&] {
-    const ulonglong2 *tg = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
-    if (threadIdx.x < N1) stw[threadIdx.x] = tg[threadIdx.x];
-    __syncthreads();
-  };
-  if (INV && !NTTB_COL_INV_LOADS_FIRST) stage_tw();
-#endif
-  u64 x[V][N1];
-#pragma unroll
-  for (int e = 0; e < N1; ++e) {
-    const long long o = static_cast<long long>(e) << COL_LOG_R;
-    if (V == 2) {
-      const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(src + o);
-      x[0][e] = v.x;
-      x[V - 1][e] = v.y;
-    } else {
-      x[0][e] = ldg_hint<L2_FIRST>(src + o);
-    }
-  }
-#if NTTB_COL_SMEM_TW
-  if (!INV || NTTB_COL_INV_LOADS_FIRST) stage_tw();
-#endif
-#if NTTB_COL_SMEM_TW
-  const ulonglong2 *twc = stw;
-#else
-  const ulonglong2 *twc = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
-#endif
-  if constexpr (LOG_N1 == 5 && V == 1) {
-    // 32-row columns (n = 2^17): the stage whose pairs straddle the two
-    // 16-element halves runs on the whole column, the other four stages as
-    // two radix-16 units (B0 = 2 + h) - the single 5-stage unit is not
-    // register-promoted by the compiler (its 32-word array went to local
-    // memory).  Same butterflies, twiddles and reduction parity.
-    if (!INV) {
-      const ulonglong2 w = ldtw(twc, 1);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) ct_bfly<LB, true>(x[0][e], x[0][e + 16], w.x, w.y, M);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      u64 y[1][16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) y[0][e] = x[0][16 * h + e];
-      if (!INV)
-        fwd_radix<LB, 4, 4, 1, 1>(y, 2 + h, twc, M);
-      else
-        inv_radix<LB, 4, 4, 0, 1>(y, 2 + h, twc, M);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) x[0][16 * h + e] = y[0][e];
-    }
-    if (INV) inv_stage0<LB, LOG_N1, V>(x, 1, twc, L, M, P.fin);
-  } else if (!INV) {
-    fwd_radix<LB, LOG_N1, LOG_N1, V>(x, 1, twc, M);
-  } else {
-    const ulonglong2 *twi = twc;
-    inv_radix<LB, LOG_N1, LOG_N1, 1, V>(x, 1, twi, M);
-    inv_stage0<LB, LOG_N1, V>(x, 1, twi, L, M, P.fin);
-  }
-  if (P.discard_src && (threadIdx.x & (16 / V - 1)) == 0) {
-    // these 16/V lanes consumed whole 128-byte lines (16 columns x N1 rows)
-#pragma unroll
-    for (int e = 0; e < N1; ++e) discard_line(src + (static_cast<long long>(e) << COL_LOG_R));
-  }
-#pragma unroll
-  for (int e = 0; e < N1; ++e) {
-    const long long o = static_cast<long long>(e) << COL_LOG_R;
-    if (V == 2) {
-      *reinterpret_cast<ulonglong2 *>(dst + o) = make_ulonglong2(x[0][e], x[V - 1][e]);
-    } else {
-      if (INV)
-        stg_hint<L2_FIRST>(dst + o, x[0][e]);  // the product: not read again here
-      else
-        stg_hint<L2_LAST>(dst + o, x[0][e]);   // a', b': the row kernel reads them next
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// PIPELINED COLUMN kernel (default for n > 4096).
-//
-// The plain column kernel above is latency-bound: each thread's 2 x N1
-// strided loads must land before any arithmetic, and 128 registers per
-// thread cap residency at 16 warps per SM.  Here a persistent CTA streams
-// column TILES (N1 rows x TC columns, rows contiguous TC*8-byte segments)
-// through a STAGES-deep shared-memory ring with the bulk-copy engine
-// (cp.async.bulk global->shared, completion counted on an mbarrier), so
-// the next tiles are in flight while the current one is transformed; results
-// go back through the same buffer with bulk shared->global stores.  One
-// thread owns one column (N1 values in registers); a warp reads 32
-// consecutive words of a row - conflict-free.
-
-namespace bulk {
-__device__ __forceinline__ unsigned saddr(const void *p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(u64 *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(u64 *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(u64 *bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(saddr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void load(void *dst, const void *src, unsigned bytes, u64 *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          saddr(dst)),
-      "l"(src), "r"(bytes), "r"(saddr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void store(void *dst, const void *src, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(saddr(src)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-}  // namespace bulk
-
-#ifndef NTTB_COLPIPE_TC
-#define NTTB_COLPIPE_TC 256
-#endif
-#ifndef NTTB_COLPIPE_STAGES
-#define NTTB_COLPIPE_STAGES 2
-#endif
-template <int LOG_N1>
-struct ColPipeGeom {
-  static constexpr int N1 = 1 << LOG_N1;
-  static constexpr int TC = LOG_N1 >= 5 ? 128 : NTTB_COLPIPE_TC;  // columns per tile = threads
-  static constexpr int STAGES = NTTB_COLPIPE_STAGES;
-  static constexpr int TILE_WORDS = N1 * TC;
-  static constexpr int TILES_PER_POLY = (1 << COL_LOG_R) / TC;
-  static constexpr size_t SMEM = STAGES * TILE_WORDS * sizeof(u64) + 64;  // + barriers
-};
-
-template <int LOG_N1, bool INV, int LB>
-__global__ void __launch_bounds__(ColPipeGeom<LOG_N1>::TC)
-    col_pipe_kernel(const ColParams P) {
-  using G = ColPipeGeom<LOG_N1>;
-  constexpr int N1 = G::N1, TC = G::TC, S = G::STAGES;
-  constexpr unsigned ROW_BYTES = TC * sizeof(u64);
-  extern __shared__ __align__(128) u64 csm[];
-  u64 *bars = csm + S * G::TILE_WORDS;
-  const long long per_src = P.npolys * G::TILES_PER_POLY;
-  const long long ntiles = per_src * P.nsrc;
-  // tile -> (source, polynomial, first column)
-  auto where = [&](long long t, int &which, long long &poly, int &col0) {
-    which = t >= per_src ? 1 : 0;
-    const long long r = t - (which ? per_src : 0);
-    poly = r / G::TILES_PER_POLY;
-    col0 = static_cast<int>(r % G::TILES_PER_POLY) * TC;
-  };
-  auto issue_load = [&](long long t, int s) {
-    int which, col0;
-    long long poly;
-    where(t, which, poly, col0);
-    const u64 *src = (which ? P.src1 : P.src0) + (poly << (COL_LOG_R + LOG_N1)) + col0;
-    bulk::mbar_expect_tx(bars + s, N1 * ROW_BYTES);
-#pragma unroll 1
-    for (int e = 0; e < N1; ++e)
-      bulk::load(csm + s * G::TILE_WORDS + e * TC, src + (static_cast<long long>(e) << COL_LOG_R),
-                 ROW_BYTES, bars + s);
-  };
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) bulk::mbar_init(bars + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  const ulonglong2 *tg = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
+  if (threadIdx.x < N1) stw[threadIdx.x] = tg[threadIdx.x];
   __syncthreads();
-  if (threadIdx.x == 0)
-    for (int s = 0; s < S; ++s) {
-      const long long t = blockIdx.x + static_cast<long long>(s) * gridDim.x;
-      if (t < ntiles) issue_load(t, s);
-    }
-  int it = 0;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int s = it % S;
-    int which, col0;
-    long long poly;
-    where(t, which, poly, col0);
-    int limb;
-    const Limb &L = *limb_ptr(P.limbs, poly, limb);
-    const Mod M = mod_for_stages<LB>(L.q);
-    u64 *buf = csm + s * G::TILE_WORDS;
-    bulk::mbar_wait(bars + s, (it / S) & 1);
-    u64 x[1][N1];
+  if (!INV)
+    col_fwd_stages<LB, LOG_N1>(x, stw, M);
+  else
+    col_inv_stages<LB, LOG_N1>(x, stw, L, M, P.fin);
 #pragma unroll
-    for (int e = 0; e < N1; ++e) x[0][e] = buf[e * TC + threadIdx.x];
-    if (!INV) {
-      fwd_radix<LB, LOG_N1, LOG_N1, 1>(x, 1, P.tw.fwd + limb * P.tw.stride, M);
-    } else {
-      const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
-      inv_radix<LB, LOG_N1, LOG_N1, 1, 1>(x, 1, twi, M);
-      inv_stage0<LB, LOG_N1, 1>(x, 1, twi, L, M, P.fin);
-    }
-#pragma unroll
-    for (int e = 0; e < N1; ++e) buf[e * TC + threadIdx.x] = x[0][e];
-    bulk::fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      u64 *dst = (which ? P.dst1 : P.dst0) + (poly << (COL_LOG_R + LOG_N1)) + col0;
-#pragma unroll 1
-      for (int e = 0; e < N1; ++e)
-        bulk::store(dst + (static_cast<long long>(e) << COL_LOG_R), buf + e * TC, ROW_BYTES);
-      bulk::commit();
-      // refill the buffer stored one iteration ago (its reads are done once
-      // at most the group just committed is still reading)
-      if (it >= 1) {
-        const int sp = (it - 1) % S;
-        const long long tn = t - gridDim.x + static_cast<long long>(S) * gridDim.x;
-        if (tn < ntiles) {
-          bulk::wait_read<1>();
-          issue_load(tn, sp);
-        }
-      }
-    }
-  }
-  // the last tile's buffer is never refilled; drain outstanding stores
-  if (threadIdx.x == 0) bulk::wait_all();
-}
-
-// ---------------------------------------------------------------------------
-// GROUP-PERSISTENT FUSED kernel (the fused product for n = N1 x 4096).
-//
-// The three-launch pipeline (COL -> ROW -> COL^-1) sends every intermediate
-// through HBM (72 n bytes per limb-product instead of 24 n) and runs the two
-// column launches latency-bound.  Here one cooperative launch keeps all of
-// it on chip: the resident CTAs form groups of N1; a group owns one
-// limb-product at a time and walks it through three phases separated by a
-// group barrier (release/acquire on a global counter):
-//   1. CTA i transforms column slab i (4096/N1 columns x N1 rows of a and b,
-//      read from HBM) and writes a', b' to the group's scratch;
-//   2. CTA i runs the fused row pass on row i (row stages of a, b, the
-//      Karatsuba middle and the inverse row stages) from scratch, c' over a';
-//   3. CTA i runs the inverse column stages (with the folded scale) on slab
-//      i of c' and writes c to HBM.
-// Scratch (triple-buffered per group, 3 MiB per group for n = 2^16) stays in
-// L2, and every scratch line is discarded once consumed, so HBM sees only a,
-// b (read) and c (written).  Different groups drift out of phase, so the
-// memory-bound column phases of one group overlap the integer-bound row
-// phases of the group sharing its SMs.
-
-struct GroupParams {
-  u64 *out;
-  const u64 *a;
-  const u64 *b;
-  u64 *scratch;            // groups x 3 buffers x {a', b'} x n words
-  unsigned *counters;      // two per group, zero at launch
-  TwSet tw;
-  LimbSet limbs;
-  long long npolys;
-  int groups;
-};
-
-// split group barrier: arrive (release) after a phase, wait (acquire) later,
-// so independent work can run in between
-__device__ __forceinline__ void group_arrive(unsigned *ctr) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-  }
-}
-__device__ __forceinline__ void group_wait(unsigned *ctr, unsigned target) {
-  if (threadIdx.x == 0) {
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    } while (v < target);
-    __threadfence();  // also invalidates this SM's L1 (scratch written elsewhere)
-  }
-  __syncthreads();
-}
-
-// scratch buffers of product number `it` of a group: {a' (then c'), b'}
-__device__ __forceinline__ u64 *group_buf(const GroupParams &P, int g, int it, long long n) {
-  return P.scratch + (static_cast<long long>(g) * 3 + it % 3) * 2 * n;
-}
-
-// phase 1: forward column stages of slab i of a and b -> a', b'
-template <int LOG_N1, int LB>
-__device__ __noinline__ void group_phase1(const GroupParams &P, long long p, int i, u64 *sa) {
-  constexpr int N1 = 1 << LOG_N1, N2 = 1 << COL_LOG_R, SW = N2 / N1;
-  constexpr long long N = static_cast<long long>(N1) * N2;
-  int limb;
-  const Limb &L = *limb_ptr(P.limbs, p, limb);
-  const Mod M = mod_for_stages<LB>(L.q);
-  const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
-#pragma unroll 1
-  for (int j = threadIdx.x; j < 2 * SW; j += blockDim.x) {
-    const int which = j >= SW;
-    const int col = i * SW + (j - (which ? SW : 0));
-    const u64 *src = (which ? P.b : P.a) + p * N + col;
-    u64 *dst = sa + (which ? N : 0) + col;
-    u64 x[1][N1];
-#pragma unroll
-    for (int e = 0; e < N1; ++e) x[0][e] = src[static_cast<long long>(e) * N2];
-    fwd_radix<LB, LOG_N1, LOG_N1, 1>(x, 1, twf, M);
-#pragma unroll
-    for (int e = 0; e < N1; ++e) dst[static_cast<long long>(e) * N2] = x[0][e];
-  }
-}
-
-// phase 2: the fused row pass on row i of (a', b'); c' over a'
-template <int LOG_N1, int MODE, int LB>
-__device__ __noinline__ void group_phase2(const GroupParams &P, long long p, int i, u64 *sa,
-                                          u64 *sm) {
-  using G = RowGeom<COL_LOG_R>;
-  constexpr int N1 = 1 << LOG_N1, N2 = G::N2;
-  constexpr long long N = static_cast<long long>(N1) * N2;
-  int limb;
-  const Limb &L = *limb_ptr(P.limbs, p, limb);
-  const Mod M = mod_for<LB>(L.q);
-  const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
-  const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
-  const u64 rowbase = static_cast<u64>(N1) + i;
-  const long long off = static_cast<long long>(i) * N2;
-  const u64 *sb = sa + N;
-  row_prefetch<COL_LOG_R>(sm + G::PADN, sb + off);
-  cp_async_commit();
-  head_fwd<LB, COL_LOG_R, 0, G::R(0), 1, true>(sm, sa + off, nullptr, rowbase, twf, M);
-  cp_async_wait<0>();
-  __syncthreads();
-  head_fwd<LB, COL_LOG_R, 0, G::R(0), 1, false>(sm + G::PADN, nullptr, nullptr, rowbase, twf, M);
-  __syncthreads();
-  head_fwd_all<LB, COL_LOG_R, 2, 1>(sm, nullptr, nullptr, rowbase, twf, M);
-  // b' is consumed: drop its lines from L2 without a write-back
-  constexpr int LINES = N2 * 8 / 128;
-  for (int l = threadIdx.x; l < LINES; l += blockDim.x) discard_line(sb + off + l * 16);
-  tail_pass<LB, COL_LOG_R, 2, FWD_TRUNC, true, INV_SKIP, MODE>(sm, rowbase, twf, twi, L, M);
-  row_sync<COL_LOG_R, G::S0(G::NPASS - 1)>();
-  head_inv_all<LB, COL_LOG_R, G::NPASS - 1>(sm, sa + off, rowbase, twi, L, M, FIN_LAZY);
-}
-
-// phase 3: inverse column stages (+ folded scale) of slab i of c' -> c
-template <int LOG_N1, int LB>
-__device__ __noinline__ void group_phase3(const GroupParams &P, long long p, int i, u64 *sa) {
-  constexpr int N1 = 1 << LOG_N1, N2 = 1 << COL_LOG_R, SW = N2 / N1;
-  constexpr long long N = static_cast<long long>(N1) * N2;
-  int limb;
-  const Limb &L = *limb_ptr(P.limbs, p, limb);
-  const Mod M = mod_for_stages<LB>(L.q);
-  const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
-#pragma unroll 1
-  for (int j = threadIdx.x; j < SW; j += blockDim.x) {
-    const int col = i * SW + j;
-    const u64 *src = sa + col;
-    u64 x[1][N1];
-#pragma unroll
-    for (int e = 0; e < N1; ++e) x[0][e] = src[static_cast<long long>(e) * N2];
-    inv_radix<LB, LOG_N1, LOG_N1, 1, 1>(x, 1, twi, M);
-    inv_stage0<LB, LOG_N1, 1>(x, 1, twi, L, M, FIN_SCALED_SKIP);
-    // every lane's loads have returned (their values were consumed): the
-    // 16 consecutive columns of a 128-byte line per row can be dropped
-    if ((j & 15) == 0)
-#pragma unroll
-      for (int e = 0; e < N1; ++e) discard_line(src + static_cast<long long>(e) * N2);
-    u64 *dst = P.out + p * N + col;
-#pragma unroll
-    for (int e = 0; e < N1; ++e) dst[static_cast<long long>(e) * N2] = x[0][e];
-  }
-}
-
-// Schedule per CTA (k = the group's k-th product), with split barriers so
-// independent work fills the waits:
-//   P1(0) arrive1 | for k: wait1(k) P2(k) arrive2 [P1(k+1) arrive1] wait2(k) P3(k)
-// Scratch is triple-buffered: a slow CTA may still read buffer k-1 in P3(k-1)
-// while a fast one writes buffer k+1 in P1(k+1).
-template <int LOG_N1, int MODE, int LB>
-__global__ void __launch_bounds__(RowGeom<COL_LOG_R>::T, NTTB_ROW_MINB_FUSED)
-    group_fused_kernel(const GroupParams P) {
-  constexpr int N1 = 1 << LOG_N1;
-  constexpr long long N = static_cast<long long>(N1) << COL_LOG_R;
-  extern __shared__ u64 sm[];
-  const int g = blockIdx.x / N1, i = blockIdx.x % N1;
-  if (g >= P.groups) return;
-  unsigned *ctr1 = P.counters + 2 * g, *ctr2 = ctr1 + 1;
-  unsigned t1 = 0, t2 = 0;
-  if (g < P.npolys) {
-    group_phase1<LOG_N1, LB>(P, g, i, group_buf(P, g, 0, N));
-    group_arrive(ctr1);
-    t1 += N1;
-  }
-  int k = 0;
-#ifdef NTTB_PHASE_TIMING
-#define GSTAMP(j) \
-  if (k == 4 && threadIdx.x == 0 && blockIdx.x < (1u << 16)) g_phase[blockIdx.x][j] = clock64();
-#else
-#define GSTAMP(j)
-#endif
-  for (long long p = g; p < P.npolys; p += P.groups, ++k) {
-    u64 *sa = group_buf(P, g, k, N);
-    GSTAMP(0);
-    group_wait(ctr1, t1);
-    GSTAMP(1);
-    group_phase2<LOG_N1, MODE, LB>(P, p, i, sa, sm);
-    group_arrive(ctr2);
-    GSTAMP(2);
-    t2 += N1;
-    if (p + P.groups < P.npolys) {
-      group_phase1<LOG_N1, LB>(P, p + P.groups, i, group_buf(P, g, k + 1, N));
-      group_arrive(ctr1);
-      t1 += N1;
-    }
-    GSTAMP(3);
-    group_wait(ctr2, t2);
-    GSTAMP(4);
-    group_phase3<LOG_N1, LB>(P, p, i, sa);
-    GSTAMP(5);
-  }
-#undef GSTAMP
+  for (int e = 0; e < N1; ++e) dst[static_cast<long long>(e) << COL_LOG_R] = x[0][e];
 }
 
 // ---------------------------------------------------------------------------
@@ -1531,7 +846,7 @@ __global__ void __launch_bounds__(256)
     modmul_roof_kernel(long long iters, u64 *sink, const Limb L, u64 w,
                        u64 wp) {
   u64 x[CHAINS];
-  const Mod M = (KIND >= 4 && L.q >= (1ULL << 34)) ? make_mod_fast(L.q) : make_mod(L.q);
+  const Mod M = make_mod(L.q);
   const u64 seed = (blockIdx.x * 256ULL + threadIdx.x) * 0x9E3779B97F4A7C15ULL;
 #pragma unroll
   for (int c = 0; c < CHAINS; ++c) x[c] = (seed + c * 0x632BE59BD9B4E019ULL) % L.q;
@@ -1542,31 +857,6 @@ __global__ void __launch_bounds__(256)
     } else if (KIND == 3) {  // inverse butterflies, [0, 4q)
 #pragma unroll
       for (int c = 0; c < CHAINS / 2; ++c) gs_bfly<8>(x[c], x[c + CHAINS / 2], w, wp, M);
-    } else if (KIND == 4) {  // forward butterflies, LB = 32 pattern (reduce, plain, plain)
-#pragma unroll
-      for (int c = 0; c < CHAINS / 2; ++c) {
-        ct_bfly<32, true>(x[c], x[c + CHAINS / 2], w, wp, M);
-        ct_bfly<32, false>(x[c], x[c + CHAINS / 2], w, wp, M);
-        ct_bfly<32, false>(x[c], x[c + CHAINS / 2], w, wp, M);
-      }
-    } else if (KIND == 6) {  // forward butterflies, shift-shaped moduli (LB = 33: reduce, plain)
-#pragma unroll
-      for (int c = 0; c < CHAINS / 2; ++c) {
-        ct_bfly<33, true>(x[c], x[c + CHAINS / 2], w, wp, M);
-        ct_bfly<33, false>(x[c], x[c + CHAINS / 2], w, wp, M);
-      }
-    } else if (KIND == 7) {  // inverse butterflies, shift-shaped moduli
-#pragma unroll
-      for (int c = 0; c < CHAINS / 2; ++c) {
-        gs_bfly<33, true>(x[c], x[c + CHAINS / 2], w, wp, M);
-        gs_bfly<33, false>(x[c], x[c + CHAINS / 2], w, wp, M);
-      }
-    } else if (KIND == 5) {  // inverse butterflies, LB = 32 pattern (reduce, plain)
-#pragma unroll
-      for (int c = 0; c < CHAINS / 2; ++c) {
-        gs_bfly<32, true>(x[c], x[c + CHAINS / 2], w, wp, M);
-        gs_bfly<32, false>(x[c], x[c + CHAINS / 2], w, wp, M);
-      }
     } else {
 #pragma unroll
       for (int c = 0; c < CHAINS; ++c) {

@@ -45,7 +45,7 @@ __device__ __forceinline__ void fwd_radix(u64 (&x)[NP][1 << R], u64 B0,
         const int i0 = gi * 2 * half + e;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          if ((LB >= 32 && NTTB_LB32_STAGES) ? (t % 3 == 0) : (((PAR + t) & 1) == 0))
+          if (((PAR + t) & 1) == 0)
             ct_bfly<LB, true>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
           else
             ct_bfly<LB, false>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
@@ -114,7 +114,7 @@ __device__ __forceinline__ void fwd_radix_pf(u64 (&x)[NP][1 << R], const TwBuf<0
         const int i0 = gi * 2 * half + e;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          if ((LB >= 32 && NTTB_LB32_STAGES) ? (t % 3 == 0) : (((PAR + t) & 1) == 0))
+          if (((PAR + t) & 1) == 0)
             ct_bfly<LB, true>(x[p][i0], x[p][i0 + half], w.x, w.y, M);
           else
             ct_bfly<LB, false>(x[p][i0], x[p][i0 + half], w.x, w.y, M);

@@ -29,6 +29,8 @@ the sweeps' ``tallies`` (uint64[3][4]) are accumulated like the reference.
 
 from __future__ import annotations
 
+import weakref
+
 import numpy as np
 import torch
 
@@ -41,34 +43,68 @@ RED_BUILTIN, RED_TWO_SUB, RED_ONE_SUB = 0, 1, 2
 
 # ---------------------------------------------------------------------------
 # twiddle pair tables: {w, floor(w 2^64 / q)} per entry, cached per table
+#
+# Entries are keyed by the identity of the caller's table (a CUDA tensor or a
+# numpy array) and evicted when that table is garbage-collected
+# (weakref.finalize), so the cache never keeps a plan's tables alive.  A
+# device table is re-paired when its torch version counter moved (in-place
+# edit); a host table when its contents differ from the copy taken when it
+# was paired (the reference passes plain ndarrays on every call, so a numpy
+# caller pays one host compare instead of an upload + pairing launch).  At
+# most _PAIRS_MAX foreign tables are cached (oldest dropped first).
 
 _PAIRS: dict = {}
+_PAIRS_MAX = 64
 
 
-def _key(t: torch.Tensor, q: int):
-    return (t.data_ptr(), t.numel(), q)
+def _evict(key) -> None:
+    _PAIRS.pop(key, None)
+
+
+def _remember(tw, q: int, entry) -> None:
+    key = (id(tw), q, torch.cuda.current_device())
+    if key not in _PAIRS:
+        while len(_PAIRS) >= _PAIRS_MAX:
+            _PAIRS.pop(next(iter(_PAIRS)))
+        weakref.finalize(tw, _evict, key)
+    _PAIRS[key] = entry
 
 
 def register_pairs(tw: torch.Tensor, pairs: torch.Tensor, q: int, w1: int) -> None:
-    """Record the pair table (and tw[1]) that belongs to device table ``tw``."""
-    _PAIRS[_key(tw, q)] = (tw._version, pairs, w1, tw)
+    """Record the pair table (and tw[1]) that belongs to device table ``tw``
+    (the caller - a plan - owns both; the cache holds no strong reference)."""
+    _remember(tw, q, (tw._version, weakref.ref(pairs), w1, None))
+
+
+def _lookup(tw, q: int):
+    hit = _PAIRS.get((id(tw), q, torch.cuda.current_device()))
+    if hit is None:
+        return None
+    version, pref, w1, host_copy = hit
+    pairs = pref() if isinstance(pref, weakref.ref) else pref
+    if pairs is None:
+        return None
+    if isinstance(tw, torch.Tensor):
+        return (pairs, w1) if version == tw._version else None
+    return (pairs, w1) if host_copy.shape == tw.shape and np.array_equal(host_copy, tw) else None
 
 
 def _pairs_for(tw, q: int):
     """(pairs tensor, tw[1]) for a twiddle table given as tensor or ndarray."""
-    if isinstance(tw, torch.Tensor) and tw.is_cuda:
-        hit = _PAIRS.get(_key(tw, q))
-        if hit is not None and hit[0] == tw._version:
-            return hit[1], hit[2]
-        t = _device.to_device(tw)
-    else:
-        t = _device.to_device(tw)
+    cacheable = (isinstance(tw, torch.Tensor) and tw.is_cuda) or isinstance(tw, np.ndarray)
+    if cacheable:
+        hit = _lookup(tw, q)
+        if hit is not None:
+            return hit
+    t = _device.to_device(tw)
     pairs = torch.empty((t.numel(), 2), dtype=_device.U64, device=t.device)
     _lib.call("nttmul_shoup_pairs", pairs.data_ptr(), t.data_ptr(), q, t.numel(),
               _device.stream_ptr())
     w1 = int(t[1].item()) if t.numel() > 1 else 1
     if isinstance(tw, torch.Tensor) and tw.is_cuda:
-        register_pairs(tw, pairs, q, w1)
+        _remember(tw, q, (tw._version, pairs, w1, None))
+    elif isinstance(tw, np.ndarray):
+        _remember(tw, q, (None, pairs, w1, np.array(tw, dtype=np.uint64, copy=True)))
     return pairs, w1
 
 

@@ -116,10 +116,12 @@ class NttPlan:
         self.n, self.log_n, self.mod = n, log_n, mod
         self.psi, self.psi_inv, self.omega, self.n_inv = psi, psi_inv, omega, n_inv
         self.reduction_variant = reduction_variant
-        self._tw_fwd = None if tw_fwd is None else _device.to_device(tw_fwd)
-        self._tw_inv = None if tw_inv is None else _device.to_device(tw_inv)
-        self._pairs = None
-        self._limb_dev = None
+        # explicit tables (possibly corrupted, for validate_plan) as given;
+        # None -> generated on the device from psi
+        self._tw_src = None if tw_fwd is None else (_device.to_device(tw_fwd),
+                                                    _device.to_device(tw_inv))
+        # per CUDA device: (tw_fwd, tw_inv, fwd_pairs, inv_pairs, limb bytes)
+        self._dev_tables: dict = {}
         self._cache: dict = {}
 
     # -- scalars ----------------------------------------------------------
@@ -137,55 +139,58 @@ class NttPlan:
         """tw_inv[1] = psi^-(n/2) (the last GS stage's twiddle)."""
         return pow(self.psi_inv, self.n // 2, self.q) if self.n >= 2 else 1
 
-    # -- device tables --------------------------------------------------
-    def _materialise(self) -> None:
-        if self._tw_fwd is not None and self._pairs is not None:
-            return
+    # -- device tables (one set per CUDA device) ---------------------------
+    def _tables(self) -> tuple:
         dev = _device.device()
+        t = self._dev_tables.get(dev.index)
+        if t is not None:
+            return t
         st = _device.stream_ptr()
         n = self.n
         fwd_pairs = torch.empty((n, 2), dtype=_device.U64, device=dev)
         inv_pairs = torch.empty((n, 2), dtype=_device.U64, device=dev)
-        if self._tw_fwd is None:
-            self._tw_fwd = torch.empty(n, dtype=_device.U64, device=dev)
-            self._tw_inv = torch.empty(n, dtype=_device.U64, device=dev)
-            _lib.call("nttmul_twiddle_tables", self._tw_fwd.data_ptr(),
-                      self._tw_inv.data_ptr(), fwd_pairs.data_ptr(), inv_pairs.data_ptr(),
-                      self.q, self.psi, self.psi_inv, self.log_n, st)
+        if self._tw_src is None:
+            tw_fwd = torch.empty(n, dtype=_device.U64, device=dev)
+            tw_inv = torch.empty(n, dtype=_device.U64, device=dev)
+            _lib.call("nttmul_twiddle_tables", tw_fwd.data_ptr(), tw_inv.data_ptr(),
+                      fwd_pairs.data_ptr(), inv_pairs.data_ptr(), self.q, self.psi,
+                      self.psi_inv, self.log_n, st)
         else:  # explicit (possibly corrupted) tables: pair them as given
-            _lib.call("nttmul_shoup_pairs", fwd_pairs.data_ptr(), self._tw_fwd.data_ptr(),
+            tw_fwd, tw_inv = (x.to(dev) for x in self._tw_src)
+            _lib.call("nttmul_shoup_pairs", fwd_pairs.data_ptr(), tw_fwd.data_ptr(),
                       self.q, n, st)
-            _lib.call("nttmul_shoup_pairs", inv_pairs.data_ptr(), self._tw_inv.data_ptr(),
+            _lib.call("nttmul_shoup_pairs", inv_pairs.data_ptr(), tw_inv.data_ptr(),
                       self.q, n, st)
-        self._pairs = (fwd_pairs, inv_pairs)
+        raw = bytes(self.limb())
+        limb = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
+        t = (tw_fwd, tw_inv, fwd_pairs, inv_pairs, limb)
+        self._dev_tables[dev.index] = t
         from . import kernels
 
-        kernels.register_pairs(self._tw_fwd, fwd_pairs, self.q, w1=1)
-        kernels.register_pairs(self._tw_inv, inv_pairs, self.q, w1=self.w1_inv)
+        kernels.register_pairs(tw_fwd, fwd_pairs, self.q, w1=1)
+        kernels.register_pairs(tw_inv, inv_pairs, self.q, w1=self.w1_inv)
+        return t
 
     @property
     def tables_ready(self) -> bool:
-        return self._pairs is not None
+        return torch.cuda.is_available() and \
+            torch.cuda.current_device() in self._dev_tables
 
     @property
     def tw_fwd(self) -> torch.Tensor:
-        self._materialise()
-        return self._tw_fwd
+        return self._tables()[0]
 
     @property
     def tw_inv(self) -> torch.Tensor:
-        self._materialise()
-        return self._tw_inv
+        return self._tables()[1]
 
     @property
     def fwd_pairs(self) -> torch.Tensor:
-        self._materialise()
-        return self._pairs[0]
+        return self._tables()[2]
 
     @property
     def inv_pairs(self) -> torch.Tensor:
-        self._materialise()
-        return self._pairs[1]
+        return self._tables()[3]
 
     def limb(self) -> "_lib.LimbStruct":
         """Host nttmul_limb_t for this plan."""
@@ -193,12 +198,8 @@ class NttPlan:
         return _lib.prepare_limb(q, mode, mu, s_in, s_out, self.log_n, self.w1_inv)
 
     def limb_device(self) -> torch.Tensor:
-        """Device copy of :meth:`limb` (96 bytes)."""
-        if self._limb_dev is None:
-            raw = bytes(self.limb())
-            self._limb_dev = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(
-                _device.device())
-        return self._limb_dev
+        """Device copy of :meth:`limb` (96 bytes) on the current device."""
+        return self._tables()[4]
 
     def __repr__(self) -> str:
         return (f"NttPlan(n={self.n}, q={self.q}, psi={self.psi}, "
@@ -253,7 +254,7 @@ def validate_plan(plan: NttPlan, tables: bool | None = None) -> None:
     if plan.omega != plan.psi * plan.psi % q:
         raise ParameterError("omega is not psi^2")
     if tables is None:
-        tables = plan._tw_fwd is not None
+        tables = plan._tw_src is not None
     if not tables:
         return
     f, v = plan.tw_fwd, plan.tw_inv

@@ -49,12 +49,13 @@ class FusedPlan:
 
     @classmethod
     def from_plan(cls, plan: NttPlan) -> "FusedPlan":
-        cached = plan._cache.get("fused")
+        key = ("fused", _device.device().index)  # views of this device's tables
+        cached = plan._cache.get(key)
         if cached is None:
             h = plan.n // 2
             cached = cls(base=plan, tw_fwd_half=plan.tw_fwd[:h], tw_inv_half=plan.tw_inv[:h],
                          fwd_pairs_half=plan.fwd_pairs[:h], inv_pairs_half=plan.inv_pairs[:h])
-            plan._cache["fused"] = cached
+            plan._cache[key] = cached
         return cached
 
 
@@ -182,13 +183,6 @@ MODE_NARROW60 = 0x200  # NTTMUL_MODE_NARROW60: every modulus < 2^60 ([0, 16q) fo
 
 
 MODE_WIDE35 = 0x400    # NTTMUL_MODE_WIDE35: every modulus >= 2^34 (multiply-based reductions)
-MODE_PM = 0x800        # NTTMUL_MODE_PM: every hi32(2^64 - q) = 2^32 - 2^s (shift-shaped)
-
-
-def shift_shaped(q: int) -> bool:
-    """hi32(2^64 - q) == 2^32 - 2^s for some s (nttmul_b200.h NTTMUL_MODE_PM)."""
-    d = (1 << 32) - (((1 << 64) - q) >> 32)
-    return 0 < d < (1 << 32) and d & (d - 1) == 0
 
 
 def mode_flags(mode: int, primes) -> int:
@@ -196,8 +190,6 @@ def mode_flags(mode: int, primes) -> int:
     top = max(primes)
     if top < (1 << 60):
         wide = MODE_WIDE35 if min(primes).bit_length() >= 35 else 0
-        if wide and all(shift_shaped(q) for q in primes):
-            wide |= MODE_PM
         return mode | MODE_NARROW | MODE_NARROW60 | wide
     return mode | (MODE_NARROW if top < (1 << 61) else 0)
 

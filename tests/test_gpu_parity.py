@@ -239,28 +239,25 @@ def test_rns_cfg3_one_ciphertext(golden):
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("log_n,limbs,batch", [(14, 8, 40), (16, 21, 4), (17, 32, 2)])
-def test_group_persistent_schedule(log_n, limbs, batch):
-    """The single cooperative group-persistent launch (large batches) and the
-    three-launch pipeline give identical products, equal to the oracle."""
+@pytest.mark.parametrize("log_n,limbs,batch", [(14, 8, 40), (16, 21, 7), (17, 32, 5)])
+def test_split_stream_schedule(log_n, limbs, batch):
+    """Large batches (>= 128 limb-products) run as two halves on internal
+    streams with event fork/join (capi.cu run_polymul); the halves cut
+    through a ciphertext when batch * limbs is odd.  The product equals the
+    per-ciphertext (unsplit) calls and the oracle."""
     basis = nt.RnsBasis.build(1 << log_n, 60, limbs, seed=0)
     n = 1 << log_n
     A = np.stack([np.stack([rand(q, n, 13 * b + l) for l, q in enumerate(basis.primes)])
                   for b in range(batch)])
     Bm = np.stack([np.stack([rand(q, n, 4099 + 13 * b + l) for l, q in enumerate(basis.primes)])
                    for b in range(batch)])
-    lib = nt._lib
-    try:
-        lib.call("nttmul_set_group", 0)
-        three = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
-        lib.call("nttmul_set_group", 1)
-        group = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
-    finally:
-        lib.call("nttmul_set_group", 0)
-    assert np.array_equal(group, three)
+    whole = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
+    each = np.stack([host(nt.polymul_rns_batch(dev(A[b:b + 1]), dev(Bm[b:b + 1]), basis))[0]
+                     for b in range(batch)])
+    assert np.array_equal(whole, each)
     k = 1 if log_n >= 16 else batch  # oracle on a subset at the large sizes
-    want = oracle.polymul_rns(A[:k], Bm[:k], basis.primes, [p.psi for p in basis.plans])
-    assert np.array_equal(group[:k], want)
+    want = oracle.polymul_rns(A[-k:], Bm[-k:], basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(whole[-k:], want)
 
 
 def test_rns_host_buffers_streamed(golden):
@@ -361,28 +358,6 @@ def test_batch_ntt_deterministic_any_workers():
     for w in (2, 8):
         out = nt.batch_ntt([r.copy() for r in rows], plan, w)
         assert all(np.array_equal(x, y.numpy()) for x, y in zip(base, out))
-
-
-@pytest.mark.parametrize("log_n,waves,B", [(16, 1, 2), (17, 1, 2), (14, 1, 3), (13, 2, 5),
-                                           (16, 0, 2)])
-def test_rns_chunked_pipeline_vs_oracle(log_n, waves, B):
-    """L2-resident chunked pipeline: chunks not aligned to ciphertexts (limb
-    offset per chunk), partial last chunk, scratch discard - all bit-exact."""
-    from paper_2209_01290_b200 import _lib
-
-    n = 1 << log_n
-    basis = nt.RnsBasis.build(n, 60, 5, seed=1)
-    A = np.stack([np.stack([rand(q, n, 31 * b + l) for l, q in enumerate(basis.primes)])
-                  for b in range(B)])
-    Bm = np.stack([np.stack([rand(q, n, 77 + 31 * b + l) for l, q in enumerate(basis.primes)])
-                   for b in range(B)])
-    want = oracle.polymul_rns(A, Bm, basis.primes, [p.psi for p in basis.plans])
-    try:
-        _lib.call("nttmul_set_pipeline", waves, 0)
-        got = host(nt.polymul_rns_batch(dev(A), dev(Bm), basis))
-    finally:
-        _lib.call("nttmul_set_pipeline", 0, 0)
-    assert np.array_equal(got, want)
 
 
 @pytest.mark.parametrize("bits", [24, 30, 59, 60, 61, 62])

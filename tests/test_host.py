@@ -293,3 +293,19 @@ def test_shoup4_bound_and_congruence(bits):
             r = _shoup4_host(x, w, wp, q)
             assert r < 4 * q
             assert r % q == x * w % q
+
+
+def test_mixed_variant_basis_accepted():
+    """The reference's RnsBasis.from_plans accepts plans of different
+    reduction variants (rns.py:61-73); the device launch then runs every limb
+    with one variant (identical canonical residues)."""
+    n = 1 << 13
+    primes = nt.RnsBasis.build(n, 60, 3, seed=0).primes
+    mixed = nt.RnsBasis.from_plans([nt.build_plan(n, q, seed=0, variant=v)
+                                    for q, v in zip(primes, ["classical", "dhem", "builtin"])])
+    assert mixed.device_variant == "proposed"
+    assert mixed.mode & 0xFF == 2  # the proposed variant's one-subtraction mode
+    same = nt.RnsBasis.from_plans([nt.build_plan(n, q, seed=0, variant="classical")
+                                   for q in primes])
+    assert same.device_variant == "classical" and same.mode & 0xFF == 1
+

@@ -134,24 +134,3 @@ def test_reduce2q_range(q):
                         else rng.randrange(1 << 64), M64, 0, q - 1, q, 2 * q - 1, 2 * q])
         y = reduce2q(x, q, r, s)
         assert y % q == x % q and y < 2 * q, (x, y)
-
-
-def test_shift_shaped_moduli():
-    """NTTMUL_MODE_PM (modarith.cuh mad_nqh / reduce2q<true>): for moduli with
-    hi32(2^64 - q) = 2^32 - 2^s the IMAD by that word equals a shift, and
-    hi32(q) = 2^s - 1.  The BASELINE primes are all of this shape (s = 28)."""
-    from paper_2209_01290_b200.polymul import shift_shaped
-    from paper_2209_01290_b200.rns import RnsBasis
-
-    primes = list(RnsBasis.build(1 << 16, 60, 21, seed=0).primes)
-    assert all(shift_shaped(q) for q in primes)
-    assert shift_shaped((1 << 61) - 1) and not shift_shaped(0x0F00000000000001)
-    rng = random.Random(5)
-    for q in primes:
-        nqh = hi((-q) & M64)
-        s = ((1 << 32) - nqh).bit_length() - 1
-        assert s == 28 and hi(q) == (1 << s) - 1
-        for _ in range(2000):
-            x, h = rng.getrandbits(32), rng.getrandbits(32)
-            assert (h + x * nqh) & M32 == (h - (x << s)) & M32
-            assert (x * hi(q)) & M32 == ((x << s) - x) & M32
