@@ -45,6 +45,9 @@ def parse():
                     help="target CPU work for the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", choices=("ct", "limb"), default=None,
+                    help="multi-GPU partition: by ciphertext (default; weak scaling) or by "
+                         "limb (default for cfg4; strong scaling)")
     return ap.parse_args()
 
 
@@ -98,7 +101,8 @@ class ClockSampler:
                     except AttributeError:
                         rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                     self.rows.append([str(sm), str(mx), hex(rs)] +
-                                     ["Active" if rs & b else "Not Active" for b in self.NVML_BITS])
+                                     ["Active" if rs & b else "Not Active" for b in self.NVML_BITS]
+                                     + [time.perf_counter()])
                     self._stop.wait(0.002)
                 return
             except Exception:  # noqa: BLE001 - fall through to nvidia-smi
@@ -110,12 +114,19 @@ class ClockSampler:
                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
                     timeout=5).stdout.strip()
                 if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                    self.rows.append([x.strip() for x in out.split(",")] + [time.perf_counter()])
             except Exception:  # noqa: BLE001 - sampling is best-effort
                 return
             self._stop.wait(0.1)
 
+    def mark_start(self):
+        self._t0 = time.perf_counter()
+
+    def mark_end(self):
+        self._t1 = time.perf_counter()
+
     def __enter__(self):
+        self._t0 = self._t1 = None
         self._nv, self._h = self._nvml_handle()  # NVML init outside the region
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
@@ -133,27 +144,36 @@ class ClockSampler:
             self._t.join(timeout=10)
 
     def summary(self) -> dict:
-        if not self.rows:
+        """Samples taken inside the marked timed region (the one nearest to
+        it when the region is shorter than the sampling period)."""
+        rows = self.rows
+        if rows and self._t0 is not None and self._t1 is not None:
+            inside = [r for r in rows if self._t0 <= r[-1] <= self._t1]
+            rows = inside or [min(rows, key=lambda r: abs(r[-1] - self._t0))]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
-        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()),
+        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in rows if r[1].replace(".", "").isdigit()),
                  default=None)
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7])
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7])
                           if v.lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": reasons, "samples": len(self.rows), "source": self.source}
+                "reasons": reasons, "samples": len(rows), "source": self.source}
 
 
 # ---------------------------------------------------------------------------
 # workload
 
-def make_inputs(primes, batch: int, n: int, seed: int):
+def make_inputs(primes, batch: int, n: int, seed: int, limb0: int = 0):
+    """[batch, len(primes), n] uniform residues; limb l (global index
+    limb0 + l) has its own generator, so a limb shard of the job holds
+    exactly the rows of the whole job."""
     import numpy as np
 
-    rng = np.random.default_rng(seed)
     out = np.empty((batch, len(primes), n), dtype=np.uint64)
     for li, q in enumerate(primes):
+        rng = np.random.default_rng([seed, limb0 + li])
         out[:, li, :] = rng.integers(0, q, size=(batch, n), dtype=np.uint64)
     return out
 
@@ -173,9 +193,48 @@ def row_kernel_modmuls(n: int) -> int:
     return 2 * (n // 2) * (l2 - 1) + 2 * n + (n // 2) * (l2 - 1)
 
 
-def cpu_reference_rate(basis_primes, psis, n, A, B, seconds: float, threads: int):
+def shard_mode(args) -> str:
+    """ct: every rank owns its own ciphertexts (weak scaling, cfg3);
+    limb: every rank owns a contiguous limb span of ONE job (strong
+    scaling, cfg4 "sharded by limb", reference rns.py:116-119)."""
+    if args.shard:
+        return args.shard
+    return "limb" if (args.log_n, args.limbs) == (17, 32) else "ct"
+
+
+def config_dict(args, world: int) -> dict:
+    """The config both arms report (identical dicts, so the driver can match
+    them)."""
+    n, L = 1 << args.log_n, args.limbs
+    mode = shard_mode(args)
+    glob = args.batch * world if mode == "ct" else args.batch
+    return {"workload": f"{CFG_NAMES.get((args.log_n, L), 'custom')}: fused negacyclic "
+                        f"polymul, N=2^{args.log_n}, {L} x 60-bit RNS limbs",
+            "n": n, "limbs": L, "global_batch": glob,
+            "batch_per_gpu": args.batch if mode == "ct" else None,
+            "parallelism": (f"shard-by-ciphertext x{world}" if mode == "ct"
+                            else f"shard-by-limb x{world}"),
+            "l2": "inputs 2x%.0f MiB per GPU > 126 MB L2, no flush" %
+                  (args.batch * L * n * 8 / 2**20 / (1 if mode == "ct" else world))}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference_rate(basis_primes, psis, n, A, B, seconds: float, threads: int,
+                       ndarray: bool = False):
     """Reference CPU polymul_fused (oracle/_ref, native Cython, GIL released)
-    over a bounded sample; returns (ct/s, kind, cores, sample, outputs)."""
+    over a bounded sample; returns (ct/s, kind, cores, sample, outputs).
+    ndarray=True passes plain ndarrays (the reference converts them through
+    _as_coeffs, polymul.py:64) instead of Polynomial objects."""
     import numpy as np
     from concurrent.futures import ThreadPoolExecutor
 
@@ -192,6 +251,8 @@ def cpu_reference_rate(basis_primes, psis, n, A, B, seconds: float, threads: int
             fplans.append(nt.FusedPlan.from_plan(plan))
 
         def one(bi, li):
+            if ndarray:
+                return nt.polymul_fused(A[bi, li], B[bi, li], fplans[li])
             return nt.polymul_fused(nt.Polynomial(A[bi, li]), nt.Polynomial(B[bi, li]),
                                     fplans[li])
     else:
@@ -224,19 +285,59 @@ def cpu_reference_rate(basis_primes, psis, n, A, B, seconds: float, threads: int
     dt, _ = run(nct)
     rate = nct / dt
     sample = (f"{nct} ciphertext(s) x {L} limbs of N={n} via "
-              f"{'nttmul.polymul_fused(Polynomial, Polynomial, FusedPlan)' if kind == 'reference' else 'oracle C port'}"
+              f"{('nttmul.polymul_fused(ndarray, ndarray, FusedPlan)' if ndarray else 'nttmul.polymul_fused(Polynomial, Polynomial, FusedPlan)') if kind == 'reference' else 'oracle C port'}"
               f", {threads} threads, {dt:.2f} s")
     first = np.stack([outs[(0, li)] for li in range(L)])
     return rate, kind, threads, sample, first
 
 
+def cpu_baseline_full(primes, psis, n, A, B, seconds: float):
+    """BASELINE.md §3's CPU figure: all host threads (best of 3), one thread,
+    and the ndarray-input path, plus the CPU model.  Returns (dict, ct 0 of
+    the reference's output)."""
+    threads = len(os.sched_getaffinity(0))
+    per = max(1.0, seconds / 5)
+    runs = [cpu_reference_rate(primes, psis, n, A, B, per, threads) for _ in range(3)]
+    best = max(runs, key=lambda r: r[0])
+    one_rate, _, _, one_sample, _ = cpu_reference_rate(primes, psis, n, A, B, per, 1)
+    nd_rate, _, _, nd_sample, _ = cpu_reference_rate(primes, psis, n, A, B, per, threads,
+                                                     ndarray=True)
+    rate, kind, cores, sample, first = best
+    return ({"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": kind,
+             "sample": sample + " (best of 3)",
+             "runs": [round(r[0], 3) for r in runs],
+             "one_thread": {"value": round(one_rate, 3), "sample": one_sample},
+             "ndarray_inputs": {"value": round(nd_rate, 3), "sample": nd_sample},
+             "cpu_model": cpu_model()}, first)
+
+
 # ---------------------------------------------------------------------------
+# N-GPU launch
+
+def spawn(args) -> int:
+    """`bench.py --gpus N` without an outer launcher: start N ranks with
+    torch.distributed.run on this node (127.0.0.1) and forward their output;
+    rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     import numpy as np
 
     if args.impl == "reference":
@@ -245,14 +346,20 @@ def main():
     import torch
     import torch.distributed as dist
 
+    import oracle
     import paper_2209_01290_b200 as nt
+    from paper_2209_01290_b200.shard import shard_range, sub_basis
 
     # NTTB_BENCH_SHARE_GPU=1 (tests of the N>1 logic on a 1-GPU box only):
     # ranks share the visible GPUs round-robin and talk over gloo, since NCCL
     # refuses two ranks on one device.  Never set for a measured run.
     share = os.environ.get("NTTB_BENCH_SHARE_GPU") == "1"
+    ngpu = torch.cuda.device_count()
     if share:
-        local = local % torch.cuda.device_count()
+        local = local % ngpu
+    elif world > ngpu:
+        raise SystemExit(f"bench.py: {world} ranks but {ngpu} visible GPU(s) "
+                         "(NTTB_BENCH_SHARE_GPU=1 shares them, logic tests only)")
     torch.cuda.set_device(local)
     if world > 1:
         if share:
@@ -260,12 +367,31 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     red_dev = "cpu" if share else "cuda"
-    n, L, Bn = 1 << args.log_n, args.limbs, args.batch
-    basis = nt.RnsBasis.build(n, 60, L, seed=0)
+
+    def allreduce(x: float, op) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    n, L_all = 1 << args.log_n, args.limbs
+    mode = shard_mode(args)
+    full = nt.RnsBasis.build(n, 60, L_all, seed=0)
+    if mode == "ct":
+        basis, lo, hi = full, 0, L_all
+        Bn = args.batch                       # this rank's ciphertexts
+        seeds = (1000 + rank, 2000 + rank)
+        cts_per_step = world * Bn             # whole job
+    else:
+        basis, lo, hi = sub_basis(full, world, rank)
+        Bn = args.batch                       # every rank: all ciphertexts, its limbs
+        seeds = (1000, 2000)
+        cts_per_step = Bn
+    L = hi - lo
     primes = list(basis.primes)
     psis = [p.psi for p in basis.plans]
-    A_h = make_inputs(primes, Bn, n, seed=1000 + rank)
-    B_h = make_inputs(primes, Bn, n, seed=2000 + rank)
+    A_h = make_inputs(primes, Bn, n, seeds[0], lo)
+    B_h = make_inputs(primes, Bn, n, seeds[1], lo)
     A = torch.from_numpy(A_h).cuda()
     B = torch.from_numpy(B_h).cuda()
     C = torch.empty_like(A)
@@ -286,16 +412,27 @@ def main():
 
     for _ in range(max(args.warmup, 3)):
         step()
+    torch.cuda.synchronize()
+    # every rank checks the first and last ciphertext of its shard against
+    # the C oracle (the reference restatement) before anything is timed
+    chk = [0, Bn - 1] if Bn > 1 else [0]
+    got = np.stack([C[i].cpu().numpy() for i in chk])  # (no uint64 fancy indexing on CUDA)
+    want = oracle.polymul_rns(A_h[chk], B_h[chk], primes, psis)
+    ok = allreduce(float(np.array_equal(got, want)), dist.ReduceOp.MIN if world > 1 else None)
+    if ok != 1.0:
+        raise SystemExit(f"bench.py: rank shard != oracle (rank {rank})")
     barrier()
     # ---- timed region: K full steps ----
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        clk.mark_start()
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         barrier()
+        clk.mark_end()
     ms = ev0.elapsed_time(ev1)
     # per-kernel breakdown (same stream, events between the three launches)
     log_n1 = max(args.log_n - 12, 0)
@@ -313,70 +450,71 @@ def main():
             phase_ms[nm] = phase_ms.get(nm, 0.0) + evs[k][0].elapsed_time(evs[k][1])
     phase_ms = {k: v / args.steps for k, v in phase_ms.items()}
 
-    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = allreduce(ms, dist.ReduceOp.MAX if world > 1 else None)
     ms_per_step = ms_max / args.steps
-    value = world * Bn * args.steps / (ms_max / 1e3)
+    value = cts_per_step * args.steps / (ms_max / 1e3)
 
-    # ---- int-pipe and HBM roofs (live microbenchmarks) ----
+    # ---- int-pipe and HBM roofs (live microbenchmarks), rank 0's kernels ----
     roof = modmul_roof(nt, basis, stream)
     hbm_peak, hbm_kind = peak_hbm()
     products_per_step = Bn * L
     row_ms = phase_ms["row_fused"]
     row_rate = products_per_step * row_kernel_modmuls(n) / (row_ms / 1e3) / 1e9
-    all_rate = products_per_step * modmuls_per_product(n) / (ms_per_step / 1e3) / 1e9
-    traffic = load_traffic("row_fused", products_per_step)
+    all_rate = products_per_step * modmuls_per_product(n) / (ms / args.steps / 1e3) / 1e9
+    traffic = load_traffic(products_per_step, n)
+    pipe = imad_pipe_roof(n, clk.summary().get("sm_mhz"))
     roofline = {
         "bound": "int", "kernel": "row_fused (fwd row stages a,b + Karatsuba middle + inv row stages)",
         "achieved": round(row_rate, 2), "peak": round(roof["peak"], 2), "unit": "Gmodmul/s",
-        "frac": round(row_rate / roof["peak"], 4), "traffic": traffic,
+        "frac": round(row_rate / roof["peak"], 4),
+        "traffic": traffic["row_fused"] if traffic else None,
         "peak_source": roof["source"], "roofs_gmodmul_s": roof["all"],
         "step_achieved": round(all_rate, 2), "step_frac": round(all_rate / roof["peak"], 4),
+        "imad_pipe": {**pipe, "row_frac": round(row_rate / pipe["peak_gmodmul_s"], 4),
+                      "step_frac": round(all_rate / pipe["peak_gmodmul_s"], 4)},
+        "ncu_row_kernel": ncu_row_summary(),
+        "step_traffic": traffic,
         "hbm": {
             "algorithmic_bytes_per_step": products_per_step * 24 * n,
-            "achieved_gbs": round(products_per_step * 24 * n / (ms_per_step / 1e3) / 1e9, 1),
+            "achieved_gbs": round(products_per_step * 24 * n / (ms / args.steps / 1e3) / 1e9, 1),
             "peak_gbs": hbm_peak, "peak_source": hbm_kind,
-            "frac": round(products_per_step * 24 * n / (ms_per_step / 1e3) / 1e9 / hbm_peak, 4),
+            "frac": round(products_per_step * 24 * n / (ms / args.steps / 1e3) / 1e9 / hbm_peak, 4),
         },
         "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
+        "per_rank_products_per_step": products_per_step,
     }
 
-    # ---- e2e: public API with pinned host buffers, copies inside timing ----
+    # ---- e2e: public API with host buffers, copies inside timing ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(nt, basis, A_h, B_h, args, world, stream, C)
+        e2e = run_e2e(nt, basis, A_h, B_h, args, world, stream, C, cts_per_step, allreduce)
 
-    # ---- parity spot check + CPU baseline (rank 0, N=1 only) ----
+    # ---- parity vs the reference itself + CPU baseline (rank 0, N=1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = len(os.sched_getaffinity(0))
-        rate, kind, cores, sample, first = cpu_reference_rate(
-            primes, psis, n, A_h, B_h, args.cpu_seconds, threads)
+        cpu, first = cpu_baseline_full(primes, psis, n, A_h, B_h, args.cpu_seconds)
         step()
         torch.cuda.synchronize()
         assert np.array_equal(C[0].cpu().numpy(), first), "GPU != reference CPU (ct 0)"
-        cpu = {"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": sample, "parity_ct0": "bit-exact"}
+        cpu["parity_ct0"] = "bit-exact vs the reference's own polymul_fused"
 
     ntt_us = ntt_latency_us(nt, basis.plans[0]) if rank == 0 else None
-    crt = crt_rates(nt, basis, Bn) if rank == 0 else None
+    crt = crt_rates(nt, full, min(args.batch, 16)) if rank == 0 and mode == "ct" else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u64", "data": "synthetic uniform residues (numpy default_rng), "
-                                   f"primes/psi = reference RnsBasis.build({n}, 60, {L}, seed=0)",
-            "config": {"workload": f"{CFG_NAMES.get((args.log_n, L), 'custom')}: fused "
-                                   f"negacyclic polymul, N=2^{args.log_n}, "
-                                   f"{L} x 60-bit RNS limbs",
-                       "batch_per_gpu": Bn, "global_batch": Bn * world, "n": n, "limbs": L,
-                       "parallelism": f"shard-by-ciphertext x{world}",
-                       "l2": "inputs 2x%.0f MiB > 126 MB L2, no flush" % (A.numel() * 8 / 2**20)},
+            "higher_is_better": True, "scaling": "weak" if mode == "ct" else "strong",
+            "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic uniform residues (numpy default_rng per limb), "
+                                   f"primes/psi = reference RnsBasis.build({n}, 60, {L_all}, seed=0)",
+            "config": config_dict(args, world),
+            "parity": {"checked": f"ciphertexts {chk} of every rank's shard vs the C oracle "
+                                  "(reference restatement), before timing", "ok": True},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-            "ntt_us": ntt_us, "crt": crt, "gpu_launches": args.steps * (3 if log_n1 else 1) * (2 if log_n1 and Bn * L >= 128 else 1),
+            "ntt_us": ntt_us, "crt": crt,
+            "gpu_launches": args.steps * (3 if log_n1 else 1) *
+                            (2 if log_n1 and Bn * L >= 128 else 1),
             "clocks": clk.summary(), "impl": "ours",
         }
         print(json.dumps(line), flush=True)
@@ -385,42 +523,48 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(nt, basis, A_h, B_h, args, world, stream, C_dev):
+def run_e2e(nt, basis, A_h, B_h, args, world, stream, C_dev, cts_per_step, allreduce):
+    """The same metric through the public API with HOST buffers: every step
+    copies its inputs host->device and the products back inside the timed
+    region.  Two caller types: pinned torch tensors (the streamed H2D /
+    kernels / D2H path at PCIe speed) and plain numpy arrays (the
+    reference's own operand type; the call stages them through pinned
+    memory itself)."""
     import torch
+    import torch.distributed as dist
 
     Ap = torch.from_numpy(A_h).pin_memory()
     Bp = torch.from_numpy(B_h).pin_memory()
     Cp = torch.empty_like(Ap).pin_memory()
-
-    def one():
-        # the public API with host buffers: chunked H2D / kernels / D2H overlap
-        # inside nttmul_polymul_fused_rns_host; returns when Cp holds c
-        nt.polymul_rns_batch(Ap, Bp, basis, out=Cp)
-
     steps = max(3, min(args.steps, 10))
-    for _ in range(2):
-        one()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        one()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    share = os.environ.get("NTTB_BENCH_SHARE_GPU") == "1"
-    t = torch.tensor([ms], dtype=torch.float64, device="cpu" if share else "cuda")
-    if world > 1:
-        import torch.distributed as dist
 
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            out = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return allreduce(e0.elapsed_time(e1), dist.ReduceOp.MAX if world > 1 else None), out
+
+    ms, _ = timed(lambda: nt.polymul_rns_batch(Ap, Bp, basis, out=Cp), steps)
     same = torch.equal(Cp, C_dev.cpu())  # streamed host result == device-resident result
-    return {"value": round(world * A_h.shape[0] * steps / (ms / 1e3), 2), "unit": UNIT,
+    nsteps = max(2, steps // 3)
+    ms_np, Cn = timed(lambda: nt.polymul_rns_batch(A_h, B_h, basis), nsteps)
+    same_np = torch.equal(Cn, Cp)
+    return {"value": round(cts_per_step * steps / (ms / 1e3), 2), "unit": UNIT,
             "h2d_bytes_per_step": int(A_h.nbytes + B_h.nbytes),
             "d2h_bytes_per_step": int(A_h.nbytes), "steps": steps,
-            "parity_vs_device": "bit-exact" if same else "MISMATCH",
-            "path": "polymul_rns_batch(pinned host tensors) -> nttmul_polymul_fused_rns_host (chunked H2D / fused kernels / D2H on 3 streams) -> pinned host"}
+            "parity_vs_device": "bit-exact" if same and same_np else "MISMATCH",
+            "path": "polymul_rns_batch(pinned host tensors) -> nttmul_polymul_fused_rns_host "
+                    "(chunked H2D / fused kernels / D2H on 3 streams) -> pinned host",
+            "numpy_unpinned": {"value": round(cts_per_step * nsteps / (ms_np / 1e3), 2),
+                               "steps": nsteps,
+                               "path": "polymul_rns_batch(numpy ndarrays): pin_memory staging "
+                                       "copy of a and b, then the same streamed call"}}
 
 
 def modmul_roof(nt, basis, stream):
@@ -464,18 +608,61 @@ def peak_hbm():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def load_traffic(kernel: str, products: int):
-    """DRAM bytes per launch of `kernel` at this batch, from the committed ncu
-    capture (profiles/traffic.json, bytes per limb-product), or None."""
+def load_traffic(products: int, n: int):
+    """DRAM bytes per launch of each kernel of the step at this batch, from
+    the committed ncu capture (profiles/traffic.json: bytes per
+    limb-product), their sum, and the sum's ratio to the 24n algorithmic
+    bytes (read a, b; write c); None without a capture."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
-            rec = json.load(fh).get(kernel)
+            rec = json.load(fh)
     except (OSError, ValueError):
         return None
-    if not rec:
+    kernels = ("col_fwd", "row_fused", "col_inv") if n > 4096 else ("row_fused",)
+    out = {}
+    for k in kernels:
+        r = rec.get(k)
+        if r and r.get("n", n) == n:
+            out[k] = int(r["bytes_per_product"] * products)
+    if not out:
         return None
-    return int(rec["bytes_per_product"] * products)
+    out["total"] = sum(out.values())
+    out["complete"] = len(out) - 1 == len(kernels)
+    out["ratio_to_24n"] = round(out["total"] / (24 * n * products), 3)
+    out["source"] = rec.get("source", "profiles/traffic.json")
+    return out
+
+
+def imad_pipe_roof(n: int, sm_mhz):
+    """Pipe-referenced roof, independent of this repo's own microbenchmark:
+    every integer multiply issues to the fmaheavy pipe at (measured,
+    profiles/r1/pipes_microbench.txt) 2 cycles per IMAD and 4 per IMAD.WIDE /
+    IMAD.HI warp instruction per SMSP.  The fused product needs, per
+    limb-product: 1.5n(log2 n - 1) + n Shoup twiddle products (5 WIDE + 4
+    IMAD = 28 cycles; the last inverse stage carries the folded scale),
+    1.5n lazy Barrett products (8 WIDE + 2 IMAD = 36) and 3n multiply-based
+    partial reductions (IMAD.HI + WIDE + IMAD = 10), over the reference's
+    24.5n-per-2^16 algorithmic modmul count."""
+    lg = n.bit_length() - 1
+    cycles = 28 * (1.5 * n * (lg - 1) + n) + 36 * 1.5 * n + 10 * 3 * n
+    per = cycles / modmuls_per_product(n)
+    mhz = sm_mhz or 1965.0
+    return {"peak_gmodmul_s": round(148 * 4 * 32 * mhz * 1e6 / per / 1e9, 1),
+            "fmaheavy_cycles_per_modmul": round(per, 2), "sm_mhz": mhz,
+            "model": "148 SMs x 4 SMSPs x 32 lanes x clock / fmaheavy cycles per modmul "
+                     "(multiplies only: 2 / IMAD, 4 / IMAD.WIDE or IMAD.HI)"}
+
+
+def ncu_row_summary():
+    """Counter-level evidence for the dominant kernel from the committed ncu
+    capture (profiles/r2/ncu_row.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r2", "ncu_row.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
 
 
 def crt_rates(nt, basis, batch):
@@ -604,14 +791,13 @@ def run_reference(args, rank, world):
     value = sum(rates) / len(rates)
     line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 / value, 3), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(1e3 / value, 3), "higher_is_better": True,
+            "scaling": "weak" if shard_mode(args) == "ct" else "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic uniform residues",
-            "config": {"workload": f"{CFG_NAMES.get((args.log_n, L), 'custom')}: fused "
-                                   f"negacyclic polymul, N=2^{args.log_n}, "
-                                   f"{L} x 60-bit RNS limbs", "n": n, "limbs": L},
+            "config": config_dict(args, world),
             "impl": "reference",
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
-                             "kind": kind, "sample": sample},
+                             "kind": kind, "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -246,6 +246,20 @@ int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
                                   uint64_t *dev_buf, int64_t chunk_cts,
                                   void *stream);
 
+/*
+ * Schedule of the transforms of n = 2^13 .. 2^16 (process-wide, per size):
+ * which = 0 selects the fused product (nttmul_polymul_fused_rns*), 1 the
+ * standalone ntt_ct / intt_gs.  NTTMUL_SCHED_THREE runs the column / row /
+ * column launches through HBM; NTTMUL_SCHED_CLUSTER one launch of one
+ * thread-block cluster per polynomial (the rows in distributed shared
+ * memory, 24n HBM bytes per product); NTTMUL_SCHED_AUTO (default) picks the
+ * measured-faster one.  All give identical results.
+ */
+#define NTTMUL_SCHED_AUTO 0
+#define NTTMUL_SCHED_THREE 1
+#define NTTMUL_SCHED_CLUSTER 2
+int nttmul_set_schedule(int which, int log_n, int schedule);
+
 /* ---- RNS decomposition / CRT reconstruction (rns.py:82-108) ------------- */
 
 /*

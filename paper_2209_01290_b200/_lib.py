@@ -17,6 +17,7 @@ LIB_NAME = "libnttmul_b200.so"
 LIB_PATH = os.environ.get("NTTMUL_LIB") or os.path.join(HERE, LIB_NAME)
 
 ABI_VERSION = 1
+SCHED_AUTO, SCHED_THREE, SCHED_CLUSTER = 0, 1, 2
 
 _c_u64 = ctypes.c_uint64
 _c_i64 = ctypes.c_int64
@@ -69,6 +70,7 @@ _PROTOS = {
                                     _c_int, _c_u64, _vp, _vp]),
     "nttmul_polymul_fused_rns": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                           _c_i64, _c_int, _vp, _vp]),
+    "nttmul_set_schedule": (_c_int, [_c_int, _c_int, _c_int]),
     "nttmul_polymul_fused_rns_phases": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                                  _c_i64, _c_int, _vp, _c_int, _vp]),
     "nttmul_polymul_fused_rns_host": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,

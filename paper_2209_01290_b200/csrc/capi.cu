@@ -13,6 +13,7 @@
 
 #include "nttmul_b200.h"
 #include "ntt_kernels.cuh"
+#include "cluster_kernels.cuh"
 #include "verify_kernels.cuh"
 #include "crt_kernels.cuh"
 
@@ -138,14 +139,17 @@ int launch_row_fused(int log_r, const RowParams &P, long long rows, cudaStream_t
 // ---- column kernel dispatch -------------------------------------------------
 template <bool INV, int LB>
 int launch_col(int log_n1, const ColParams &P, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>(
-      (P.nsrc * (P.npolys << COL_LOG_R) + COL_THREADS - 1) / COL_THREADS);
+  const long long total = P.nsrc * (P.npolys << COL_LOG_R);  // columns
+#define NTTB_COL(LN)                                                                   \
+  col_kernel<LN, INV, LB><<<static_cast<unsigned>(total / ColGeom<INV, LN>::SPAN), COL_THREADS, \
+                            0, st>>>(P)
   switch (log_n1) {
-    case 1: col_kernel<1, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
-    case 2: col_kernel<2, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
-    case 3: col_kernel<3, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
-    case 4: col_kernel<4, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
-    case 5: col_kernel<5, INV, LB><<<grid, COL_THREADS, 0, st>>>(P); break;
+    case 1: NTTB_COL(1); break;
+    case 2: NTTB_COL(2); break;
+    case 3: NTTB_COL(3); break;
+    case 4: NTTB_COL(4); break;
+    case 5: NTTB_COL(5); break;
+#undef NTTB_COL
     default: return fail(NTTMUL_EINVAL, "column count 2^%d unsupported", log_n1);
   }
   return cuda_status("col_kernel");
@@ -168,6 +172,81 @@ int launch_small(const SmallParams &P, int mode, long long npolys, cudaStream_t 
   return cuda_status("small_kernel");
 }
 
+// ---- cluster kernel (one thread-block cluster per polynomial) ------------
+// Schedule per transform size for n = 2^13 .. 2^16: the three-launch
+// column / row / column pipeline through HBM or the single cluster launch
+// (cluster_kernels.cuh).  Index = log_n; NTTMUL_SCHED_* values.
+int g_sched_fused[NTTMUL_MAX_LOG_N + 1] = {0};
+int g_sched_xform[NTTMUL_MAX_LOG_N + 1] = {0};
+
+template <int LOG_N1, int KIND, int MODE, int LB>
+int launch_cluster_t(const ClusterParams &P, long long npolys, cudaStream_t st) {
+  using C = ClusterGeom<LOG_N1>;
+  constexpr int NP = KIND == CL_FUSED ? 2 : 1;
+  constexpr size_t smem =
+      (KIND == CL_INV ? C::G::PADN : (NP * C::G::PADN + C::N2)) * sizeof(u64);
+  auto k = cluster_kernel<LOG_N1, KIND, MODE, LB>;
+  static bool ready = false;  // attributes set once per instantiation
+  if (!ready) {
+    CHECK(smem_optin(k, smem));
+    if (C::N1 > 8 &&
+        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+            cudaSuccess)
+      return cuda_status("cluster size 16 opt-in");
+    ready = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(npolys << LOG_N1));
+  cfg.blockDim = dim3(C::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::N1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static bool told = false;
+  if (!told && std::getenv("NTTB_DEBUG_OCC")) {
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess) cudaGetLastError();
+    std::fprintf(stderr, "cluster_kernel<%d,%d,%d,%d>: %d active clusters of %d CTAs, smem %zu\n",
+                 LOG_N1, KIND, MODE, LB, nc, C::N1, smem);
+    told = true;
+  }
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, P);
+  if (e != cudaSuccess) return fail(NTTMUL_ELAUNCH, "cluster_kernel: %s", cudaGetErrorString(e));
+  return cuda_status("cluster_kernel");
+}
+
+template <int KIND, int MODE, int LB>
+int launch_cluster(int log_n1, const ClusterParams &P, long long npolys, cudaStream_t st) {
+  if (npolys == 0) return NTTMUL_OK;
+  switch (log_n1) {
+    case 1: return launch_cluster_t<1, KIND, MODE, LB>(P, npolys, st);
+    case 2: return launch_cluster_t<2, KIND, MODE, LB>(P, npolys, st);
+    case 3: return launch_cluster_t<3, KIND, MODE, LB>(P, npolys, st);
+    case 4: return launch_cluster_t<4, KIND, MODE, LB>(P, npolys, st);
+  }
+  return fail(NTTMUL_EINVAL, "cluster schedule: 2^%d rows unsupported", log_n1);
+}
+
+// Default schedule (NTTMUL_SCHED_AUTO) per size, from the round-2
+// measurements (profiles/r2/NOTES.md).
+inline bool use_cluster(const int *table, int log_n, long long npolys) {
+  if (log_n <= COL_LOG_R || log_n > COL_LOG_R + 4) return false;
+  const int s = table[log_n];
+  if (s == NTTMUL_SCHED_THREE) return false;
+  if (s == NTTMUL_SCHED_CLUSTER) return true;
+  // auto (schedule_sweep r2, profiles/r2/NOTES.md): the cluster launch wins
+  // for n = 2^13 at any batch and for single transforms up to 2^16 (one
+  // launch, no HBM round trip: -2 us); the three launches win for the
+  // larger batched products (their column passes overlap the row kernel of
+  // the other stream half; a cluster CTA waits on its own HBM phases)
+  return log_n == COL_LOG_R + 1 || (table == g_sched_xform && npolys <= 4);
+}
+
 constexpr int SMALL_MAX_LOG = 9;  // n <= 2^9 -> small kernel
 
 // ---- composite transforms -----------------------------------------------------
@@ -182,6 +261,13 @@ int run_forward(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
   }
   const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
   const int log_n1 = log_n - log_r;
+  if constexpr (LB == 16) {  // (instantiated for the < 2^60 moduli only)
+    if (use_cluster(g_sched_xform, log_n, npolys)) {
+      ClusterParams P{a, a, nullptr, tw, ls, truncate ? FWD_TRUNC : FWD_FULL, INV_NONE,
+                      FIN_PLAIN};
+      return launch_cluster<CL_FWD, 2, LB>(log_n1, P, npolys, st);
+    }
+  }
   if (log_n1 > 0) {
     ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, FIN_LAZY};
     CHECK((launch_col<false, LB>(log_n1, C, st)));
@@ -203,6 +289,12 @@ int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
   }
   const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
   const int log_n1 = log_n - log_r;
+  if constexpr (LB == 8) {  // (the inverse of every modulus < 2^61)
+    if (use_cluster(g_sched_xform, log_n, npolys)) {
+      ClusterParams P{a, a, nullptr, tw, ls, FWD_NONE, skip ? INV_SKIP : INV_FULL, fin};
+      return launch_cluster<CL_INV, 2, LB>(log_n1, P, npolys, st);
+    }
+  }
   RowParams R{a, a, nullptr, tw, ls, log_n1, fin, 0};
   const long long rows = npolys << log_n1;
   CHECK((skip ? launch_row_m<FWD_NONE, false, INV_SKIP, 2, LB>(log_r, R, rows, st)
@@ -237,6 +329,13 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
     if (!(phases & 2)) return NTTMUL_OK;
     RowParams R{c, a, b, tw, ls, 0, FIN_SCALED_SKIP, 0};
     return launch_row_fused<MODE, LB>(log_r, R, npolys, st);
+  }
+  if constexpr (MODE == NTTMUL_RED_ONE_SUB && LB >= 16) {  // the proposed / dhem
+    // constants with every modulus < 2^60 (the BASELINE bases)
+    if (phases == 7 && use_cluster(g_sched_fused, log_n, npolys)) {
+      ClusterParams P{c, a, b, tw, ls, FWD_TRUNC, INV_SKIP, FIN_SCALED_SKIP};
+      return launch_cluster<CL_FUSED, MODE, LB>(log_n1, P, npolys, st);
+    }
   }
   if (phases & 1) {
     ColParams C{a, b, c, ws, 2, npolys, tw, ls, FIN_LAZY};
@@ -294,7 +393,9 @@ int side_streams(SideStreams **out) {
 int run_polymul(int mode, int lb, u64 *c, const u64 *a, const u64 *b, u64 *ws,
                 const TwSet &tw, const LimbSet &ls, int log_n, long long npolys,
                 int phases, cudaStream_t st) {
-  const bool split = phases == 7 && log_n > COL_LOG_R && npolys >= 64 * SPLIT_PARTS;
+  const bool split = phases == 7 && log_n > COL_LOG_R && npolys >= 64 * SPLIT_PARTS &&
+                     !(mode == NTTMUL_RED_ONE_SUB && lb >= 16 &&
+                       use_cluster(g_sched_fused, log_n, npolys));
   if (!split)
     return run_polymul_one(mode, lb, c, a, b, ws, tw, ls, log_n, npolys, phases, st);
   SideStreams *sd = nullptr;
@@ -636,6 +737,14 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
            reinterpret_cast<const ulonglong2 *>(inv_pairs), stride};
   return run_polymul(mode, lbx, c, a, b, workspace, tw, ls, log_n,
                      batch * num_limbs, phases, S(stream));
+}
+
+int nttmul_set_schedule(int which, int log_n, int schedule) {
+  if (which < 0 || which > 1 || log_n < COL_LOG_R + 1 || log_n > COL_LOG_R + 4 ||
+      schedule < NTTMUL_SCHED_AUTO || schedule > NTTMUL_SCHED_CLUSTER)
+    return fail(NTTMUL_EINVAL, "set_schedule(%d, %d, %d)", which, log_n, schedule);
+  (which == 0 ? g_sched_fused : g_sched_xform)[log_n] = schedule;
+  return NTTMUL_OK;
 }
 
 int nttmul_polymul_fused_rns(uint64_t *c, const uint64_t *a, const uint64_t *b,

@@ -598,23 +598,29 @@ __device__ __forceinline__ void col_inv_stages(u64 (&x)[1][1 << LOG_N1], const u
   inv_stage0<LB, LOG_N1, 1>(x, 1, twc, L, M, fin);
 }
 
-// Each thread owns one column (one 8-byte word per row, coalesced across
-// the warp) and runs all LOG_N1 column stages on it in registers; the
-// stages' twiddles tw[1 .. N1) are uniform across the CTA.
+// Each thread owns COLS columns (one 8-byte word per row each, coalesced
+// across the warp; the CTA's columns are first + t + k 256) and runs all
+// LOG_N1 column stages on them in registers; the stages' twiddles tw[1 ..
+// N1) are uniform across the CTA.  Short columns (N1 <= 8) take several per
+// thread so that 16 loads per thread are in flight.
 template <bool INV, int LOG_N1>
 struct ColGeom {
   // 32-word columns (n = 2^17) need the register budget of 2 CTAs/SM
   static constexpr int MINB = LOG_N1 >= 5 ? 2 : (INV ? NTTB_COL_MINB_INV : NTTB_COL_MINB);
+  static constexpr int COLS = LOG_N1 >= 4 ? 1 : (16 >> LOG_N1);
+  static constexpr int SPAN = COL_THREADS * COLS;  // columns per CTA
 };
 
 template <int LOG_N1, bool INV, int LB>
 __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col_kernel(const ColParams P) {
   constexpr int N1 = 1 << LOG_N1;
+  using CG = ColGeom<INV, LOG_N1>;
+  constexpr int COLS = CG::COLS;
   const long long cols = P.npolys << COL_LOG_R;  // columns per source
-  // a CTA's COL_THREADS columns lie in one polynomial of one source (4096
-  // columns per polynomial), so source, polynomial and limb are CTA-uniform:
-  // derive them from blockIdx only
-  const long long cta0 = blockIdx.x * static_cast<long long>(COL_THREADS);
+  // a CTA's SPAN columns lie in one polynomial of one source (4096 columns
+  // per polynomial), so source, polynomial and limb are CTA-uniform: derive
+  // them from blockIdx only
+  const long long cta0 = blockIdx.x * static_cast<long long>(CG::SPAN);
   if (cta0 >= cols * P.nsrc) return;
   const int which = cta0 >= cols ? 1 : 0;
   const long long first = cta0 - (which ? cols : 0);
@@ -632,19 +638,26 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
   // 2 x (N1 - 1) global loads into registers, and the staging barrier
   // overlaps the HBM latency (forward -4 %, then 4 CTAs/SM -15 %; inverse
   // at 4 CTAs/SM -5 %).
-  u64 x[1][N1];
+  u64 x[COLS][1][N1];
 #pragma unroll
-  for (int e = 0; e < N1; ++e) x[0][e] = src[static_cast<long long>(e) << COL_LOG_R];
+  for (int k = 0; k < COLS; ++k)
+#pragma unroll
+    for (int e = 0; e < N1; ++e)
+      x[k][0][e] = src[(static_cast<long long>(e) << COL_LOG_R) + k * COL_THREADS];
   __shared__ ulonglong2 stw[N1];
   const ulonglong2 *tg = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
   if (threadIdx.x < N1) stw[threadIdx.x] = tg[threadIdx.x];
   __syncthreads();
-  if (!INV)
-    col_fwd_stages<LB, LOG_N1>(x, stw, M);
-  else
-    col_inv_stages<LB, LOG_N1>(x, stw, L, M, P.fin);
 #pragma unroll
-  for (int e = 0; e < N1; ++e) dst[static_cast<long long>(e) << COL_LOG_R] = x[0][e];
+  for (int k = 0; k < COLS; ++k) {
+    if (!INV)
+      col_fwd_stages<LB, LOG_N1>(x[k], stw, M);
+    else
+      col_inv_stages<LB, LOG_N1>(x[k], stw, L, M, P.fin);
+#pragma unroll
+    for (int e = 0; e < N1; ++e)
+      dst[(static_cast<long long>(e) << COL_LOG_R) + k * COL_THREADS] = x[k][0][e];
+  }
 }
 
 // ---------------------------------------------------------------------------

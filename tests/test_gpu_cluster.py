@@ -1,0 +1,111 @@
+"""GPU parity of the thread-block-cluster schedule (csrc/cluster_kernels.cuh):
+one cluster of n / 4096 CTAs per polynomial, rows in distributed shared
+memory.  Forced on with nttmul_set_schedule and compared bit-for-bit with
+the C oracle and with the three-launch column / row / column schedule, for
+the fused product (n = 2^13 .. 2^16, ragged batches, every cluster size) and
+the standalone transforms (ntt_ct full / truncated, intt_gs scaled / plain /
+skip_first)."""
+
+from __future__ import annotations
+
+import contextlib
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import rand
+
+pytestmark = pytest.mark.gpu
+
+nt = pytest.importorskip("paper_2209_01290_b200")
+lib = nt._lib
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint64)).cuda()
+
+
+@contextlib.contextmanager
+def schedule(which, log_n, sched):
+    lib.call("nttmul_set_schedule", which, log_n, sched)
+    try:
+        yield
+    finally:
+        lib.call("nttmul_set_schedule", which, log_n, lib.SCHED_AUTO)
+
+
+@pytest.mark.parametrize("log_n,L,B", [(13, 3, 3), (14, 8, 5), (15, 2, 3), (16, 21, 1),
+                                       (16, 3, 6)])
+def test_cluster_fused_product(log_n, L, B):
+    n = 1 << log_n
+    basis = nt.RnsBasis.build(n, 60, L, seed=0)
+    A = np.stack([np.stack([rand(q, n, 11 * b + l) for l, q in enumerate(basis.primes)])
+                  for b in range(B)])
+    Bm = np.stack([np.stack([rand(q, n, 909 + 11 * b + l) for l, q in enumerate(basis.primes)])
+                   for b in range(B)])
+    with schedule(0, log_n, lib.SCHED_CLUSTER):
+        got = nt.polymul_rns_batch(dev(A), dev(Bm), basis).cpu().numpy()
+    with schedule(0, log_n, lib.SCHED_THREE):
+        three = nt.polymul_rns_batch(dev(A), dev(Bm), basis).cpu().numpy()
+    assert np.array_equal(got, three)
+    k = min(B, 2)
+    want = oracle.polymul_rns(A[:k], Bm[:k], basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(got[:k], want)
+
+
+def test_cluster_fused_edge_values():
+    """q - 1 everywhere and x^(n-1) * x = -1 through the cluster path."""
+    n = 1 << 14
+    basis = nt.RnsBasis.build(n, 60, 2, seed=0)
+    q = np.array(basis.primes, dtype=np.uint64)[None, :, None]
+    A = np.broadcast_to(q - 1, (1, 2, n)).copy()
+    X = np.zeros((1, 2, n), dtype=np.uint64)
+    Y = np.zeros((1, 2, n), dtype=np.uint64)
+    X[..., n - 1] = 1
+    Y[..., 1] = 1
+    with schedule(0, 14, lib.SCHED_CLUSTER):
+        got = nt.polymul_rns_batch(dev(A), dev(A), basis).cpu().numpy()
+        wrap = nt.polymul_rns_batch(dev(X), dev(Y), basis).cpu().numpy()
+    want = oracle.polymul_rns(A, A, basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(got, want)
+    assert np.array_equal(wrap[..., 0], (q - 1)[..., 0]) and not wrap[..., 1:].any()
+
+
+@pytest.mark.parametrize("log_n", [13, 14, 15, 16])
+def test_cluster_standalone_transforms(log_n):
+    n = 1 << log_n
+    plan = nt.build_plan(n, bits=59, seed=1)
+    f, v = oracle.twiddles(plan.q, plan.psi, log_n)
+    rows = np.stack([rand(plan.q, n, 7 + i) for i in range(3)])
+    args = plan.red_args
+    for truncate in (False, True):
+        want = rows.copy()
+        for w in want:
+            oracle.ntt_ct(w, f, *args, truncate)
+        x = dev(rows)
+        with schedule(1, log_n, lib.SCHED_CLUSTER):
+            nt.kernels.ntt_ct(x, plan.tw_fwd, *args, truncate, None)
+        assert np.array_equal(x.cpu().numpy(), want), f"ntt_ct truncate={truncate}"
+    half_q = (plan.q + 1) // 2
+    for scaled, skip in ((True, False), (False, False), (True, True)):
+        want = rows.copy()
+        for w in want:
+            oracle.intt_gs(w, v, plan.q, half_q, *args[1:], scaled, skip)
+        x = dev(rows)
+        with schedule(1, log_n, lib.SCHED_CLUSTER):
+            nt.kernels.intt_gs(x, plan.tw_inv, plan.q, half_q, *args[1:], scaled, skip, None)
+        assert np.array_equal(x.cpu().numpy(), want), f"intt_gs scaled={scaled} skip={skip}"
+
+
+def test_schedule_knob_rejects_bad_arguments():
+    for args in ((2, 14, 1), (0, 12, 1), (0, 17, 1), (0, 14, 3)):
+        with pytest.raises(nt._lib.NttmulError):
+            lib.call("nttmul_set_schedule", *args)
