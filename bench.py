@@ -699,6 +699,9 @@ def crt_rates(nt, basis, batch):
             "decompose_gbs": round(nbytes / (dec_ms / 1e3) / 1e9, 1),
             "reconstruct_gbs": round(nbytes / (rec_ms / 1e3) / 1e9, 1),
             "decompose_gmodmul_s": round(batch * n * L * W / (dec_ms / 1e3) / 1e9, 1),
+            "reconstruct_gmodmul_s": round(batch * n * L * W / (rec_ms / 1e3) / 1e9, 1),
+            "unit_note": "L x W word-by-constant products per coefficient (the reference's "
+                         "per-word reductions), against the same modmul roofs as the product",
             "note": f"[{batch}, {n}, {W}] words <-> [{batch}, {L}, {n}] residues, round trip exact"}
 
 

@@ -914,7 +914,11 @@ int nttmul_crt_decompose(uint64_t *res, const uint64_t *words, const uint64_t *p
   const long long total = batch * n;
   const auto *pw = reinterpret_cast<const ulonglong2 *>(word_pairs);
   const unsigned grid = grid_for(total, CRT_THREADS);
-  const size_t smem = static_cast<size_t>(CRT_THREADS) * crt_stride(num_words) * sizeof(u64);
+  const size_t smem = (static_cast<size_t>(CRT_THREADS) * crt_stride(num_words) +
+                       static_cast<size_t>(num_limbs) * num_words) * sizeof(u64) +
+                      num_limbs * sizeof(CrtLimbConsts);
+  if (smem > 200 * 1024) return fail(NTTMUL_EINVAL, "crt_decompose: L=%d W=%d too large",
+                                     num_limbs, num_words);
   CHECK(smem_optin(crt_decompose_kernel, smem));
   crt_decompose_kernel<<<grid, CRT_THREADS, smem, S(stream)>>>(res, words, primes, pw, num_limbs,
                                                                num_words, n, total);

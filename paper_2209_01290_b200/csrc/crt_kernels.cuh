@@ -25,18 +25,52 @@ namespace nttb {
 // reads / writes its own row from shared memory with an odd word stride
 // (conflict-free 8-byte accesses).
 constexpr int CRT_THREADS = 128;
-constexpr int CRT_ILP = 4;  // limbs per decompose pass
+constexpr int CRT_ILP = 7;  // limbs per decompose pass (cfg3: 21 = 3 x 7)
 __host__ __device__ constexpr int crt_stride(int W) { return W | 1; }
 
 // ---- decompose: one thread per coefficient, all limbs ----------------------
-// The thread's words stay in its shared-memory row (no register arrays, so
-// any W works without local memory).
+// c mod q = (sum_w c_w R_w) mod q with R_w = 2^(64 w) mod q: the W products
+// c_w R_w (< 2^124) are summed EXACTLY in a 128-bit accumulator with a carry
+// word (PTX mad.lo.cc / madc.hi.cc, one 64x64 multiply-add per word, no
+// reduction inside the loop), and the sum top 2^128 + hi 2^64 + lo is
+// reduced once: shoup(lo, 1) + shoup(hi, 2^64 mod q) + top (2^128 mod q),
+// canonicalised.  CRT_ILP limbs run side by side (independent carry
+// chains).  The thread's words stay in its shared-memory row, the R table
+// and the per-limb constants in shared memory (broadcast reads).
+struct CrtLimbConsts {
+  u64 q, f1;        // q, floor(2^64 / q)  (Shoup pair of the constant 1)
+  u64 t1, t1p;      // 2^64 mod q and its Shoup companion
+  u64 t2;           // 2^128 mod q
+};
+
+__device__ __forceinline__ void mac128(u64 &lo, u64 &hi, u64 &top, u64 a, u64 b) {
+  asm("mad.lo.cc.u64 %0, %3, %4, %0;\n\t"
+      "madc.hi.cc.u64 %1, %3, %4, %1;\n\t"
+      "addc.u64 %2, %2, 0;"
+      : "+l"(lo), "+l"(hi), "+l"(top)
+      : "l"(a), "l"(b));
+}
+
 __global__ void __launch_bounds__(CRT_THREADS)
     crt_decompose_kernel(u64 *__restrict__ res, const u64 *__restrict__ words,
                          const u64 *__restrict__ qs, const ulonglong2 *__restrict__ pw,
                          int L, int W, long long n, long long total) {
   extern __shared__ u64 cw[];
   const int S = crt_stride(W);
+  u64 *R = cw + CRT_THREADS * S;                                  // [L][W]
+  CrtLimbConsts *K = reinterpret_cast<CrtLimbConsts *>(R + L * W);  // [L]
+  for (int k = threadIdx.x; k < L * W; k += CRT_THREADS) R[k] = pw[k].x;
+  // the constants are entries of the word table: pw[i][w] = {2^(64 w) mod q,
+  // its Shoup companion}; hi (top) can be non-zero only when W >= 2 (3)
+  for (int i = threadIdx.x; i < L; i += CRT_THREADS) {
+    CrtLimbConsts c;
+    c.q = qs[i];
+    c.f1 = pw[i * W].y;
+    c.t1 = W >= 2 ? pw[i * W + 1].x : 0;
+    c.t1p = W >= 2 ? pw[i * W + 1].y : 0;
+    c.t2 = W >= 3 ? pw[i * W + 2].x : 0;
+    K[i] = c;
+  }
   for (long long t0 = blockIdx.x * static_cast<long long>(CRT_THREADS); t0 < total;
        t0 += static_cast<long long>(gridDim.x) * CRT_THREADS) {
     const int rows = total - t0 < CRT_THREADS ? static_cast<int>(total - t0) : CRT_THREADS;
@@ -48,30 +82,32 @@ __global__ void __launch_bounds__(CRT_THREADS)
     const long long t = t0 + threadIdx.x;
     const long long b = t / n, j = t - b * n;
     const u64 *row = cw + threadIdx.x * S;
-    // CRT_ILP limbs at a time: independent accumulator chains share each
-    // word read from shared memory
     for (int i0 = 0; i0 < L; i0 += CRT_ILP) {
-      Mod M[CRT_ILP];
-      u64 acc[CRT_ILP];
+      u64 lo[CRT_ILP], hi[CRT_ILP], top[CRT_ILP];
+      int li[CRT_ILP];
 #pragma unroll
       for (int u = 0; u < CRT_ILP; ++u) {
-        M[u] = make_mod(qs[i0 + u < L ? i0 + u : i0]);
-        acc[u] = 0;
+        li[u] = i0 + u < L ? i0 + u : i0;
+        lo[u] = hi[u] = top[u] = 0;
       }
-#pragma unroll 2
+#pragma unroll 4
       for (int w = 0; w < W; ++w) {
         const u64 c = row[w];
 #pragma unroll
-        for (int u = 0; u < CRT_ILP; ++u) {
-          const int i = i0 + u < L ? i0 + u : i0;
-          const ulonglong2 p = pw[static_cast<long long>(i) * W + w];
-          const u64 r = csub(csub(shoup4(c, p.x, p.y, M[u]), M[u].q2), M[u].q);  // [0, q)
-          acc[u] = csub(acc[u] + r, M[u].q);
-        }
+        for (int u = 0; u < CRT_ILP; ++u) mac128(lo[u], hi[u], top[u], c, R[li[u] * W + w]);
       }
 #pragma unroll
-      for (int u = 0; u < CRT_ILP; ++u)
-        if (i0 + u < L) res[(b * L + i0 + u) * n + j] = acc[u];
+      for (int u = 0; u < CRT_ILP; ++u) {
+        const CrtLimbConsts &c = K[li[u]];
+        const Mod M = make_mod(c.q);
+        // each part canonical first (q may have 62 bits); top <= 1: the sum
+        // is below 2^128.4
+        const u64 r0 = csub(csub(shoup4(lo[u], 1, c.f1, M), M.q2), M.q);
+        const u64 r1 = csub(csub(shoup4(hi[u], c.t1, c.t1p, M), M.q2), M.q);
+        u64 r = csub(r0 + r1, M.q);
+        r = csub(r + (top[u] ? c.t2 : 0), M.q);
+        if (i0 + u < L) res[(b * L + i0 + u) * n + j] = r;
+      }
     }
   }
 }
