@@ -484,6 +484,10 @@ def main():
         "per_rank_products_per_step": products_per_step,
     }
 
+    # ---- short device measurements while the GPU is still at full clock
+    # (after the multi-second CPU baseline the clocks have dropped) ----
+    ntt_us = ntt_latency_us(nt, basis.plans[0]) if rank == 0 else None
+    crt = crt_rates(nt, full, min(args.batch, 16)) if rank == 0 and mode == "ct" else None
     # ---- e2e: public API with host buffers, copies inside timing ----
     e2e = None
     if not args.no_e2e:
@@ -498,8 +502,6 @@ def main():
         assert np.array_equal(C[0].cpu().numpy(), first), "GPU != reference CPU (ct 0)"
         cpu["parity_ct0"] = "bit-exact vs the reference's own polymul_fused"
 
-    ntt_us = ntt_latency_us(nt, basis.plans[0]) if rank == 0 else None
-    crt = crt_rates(nt, full, min(args.batch, 16)) if rank == 0 and mode == "ct" else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
@@ -679,7 +681,7 @@ def crt_rates(nt, basis, batch):
     words[:, :, W - 1] = 0  # < big_q
     stream = torch.cuda.current_stream()
 
-    def timed(fn, reps=5):
+    def timed(fn, reps=20):
         fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -255,6 +255,16 @@ int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
  * memory, 24n HBM bytes per product); NTTMUL_SCHED_AUTO (default) picks the
  * measured-faster one.  All give identical results.
  */
+/*
+ * Radix split of the transforms of n = 2^13 .. 2^17 into N1 = n / 2^log_r
+ * columns x 2^log_r-word rows (process-wide, per size; three-launch
+ * schedule): log_r in 10 .. 13 with 1 <= log2(N1) <= 5, or 0 for the default
+ * 2^12 (the cluster schedule always uses 2^12).  All splits give identical
+ * results; they trade column stages (HBM round trips) against row stages
+ * (the 2^13 rows run 1024-thread CTAs at one per SM).  BASELINE cfg5 sweep.
+ */
+int nttmul_set_split(int log_n, int log_r);
+
 #define NTTMUL_SCHED_AUTO 0
 #define NTTMUL_SCHED_THREE 1
 #define NTTMUL_SCHED_CLUSTER 2

@@ -24,8 +24,14 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_ptr() -> int:
-    """cudaStream_t of torch's current stream (the launch stream)."""
+    """cudaStream_t of torch's current stream (the launch stream) - the raw
+    handle without building a torch.cuda.Stream object (a few us per call)."""
+    if _raw_stream is not None:
+        return _raw_stream(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 

@@ -71,6 +71,7 @@ _PROTOS = {
     "nttmul_polymul_fused_rns": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                           _c_i64, _c_int, _vp, _vp]),
     "nttmul_set_schedule": (_c_int, [_c_int, _c_int, _c_int]),
+    "nttmul_set_split": (_c_int, [_c_int, _c_int]),
     "nttmul_polymul_fused_rns_phases": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                                  _c_i64, _c_int, _vp, _c_int, _vp]),
     "nttmul_polymul_fused_rns_host": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,

@@ -10,6 +10,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "nttmul_b200.h"
 #include "ntt_kernels.cuh"
@@ -77,14 +81,25 @@ inline unsigned grid_for(long long n, int threads, long long cap = 148LL * 64) {
   return static_cast<unsigned>(g < 1 ? 1 : g);
 }
 
-// ---- dynamic shared memory opt-in (once per kernel instantiation) --------
+// ---- dynamic shared memory opt-in (once per kernel and device) ------------
+// cudaFuncSetAttribute costs host time on every call; remember the largest
+// size already granted per (kernel, device).
 template <class K>
 int smem_optin(K kernel, size_t bytes) {
   if (bytes <= 48 * 1024) return NTTMUL_OK;
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> granted;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(reinterpret_cast<const void *>(kernel), dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = granted.find(key);
+  if (it != granted.end() && it->second >= bytes) return NTTMUL_OK;
   const cudaError_t e = cudaFuncSetAttribute(
       kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
   if (e != cudaSuccess)
     return fail(NTTMUL_ECUDA, "smem opt-in %zu B: %s", bytes, cudaGetErrorString(e));
+  granted[key] = bytes;
   return NTTMUL_OK;
 }
 
@@ -126,6 +141,7 @@ int launch_row_m(int log_r, const RowParams &P, long long rows, cudaStream_t st)
     case 10: return launch_row_t<10, FWD, MID, INV, MODE, LB>(P, rows, st);
     case 11: return launch_row_t<11, FWD, MID, INV, MODE, LB>(P, rows, st);
     case 12: return launch_row_t<12, FWD, MID, INV, MODE, LB>(P, rows, st);
+    case 13: return launch_row_t<13, FWD, MID, INV, MODE, LB>(P, rows, st);
   }
   return fail(NTTMUL_EINVAL, "row size 2^%d unsupported", log_r);
 }
@@ -137,22 +153,54 @@ int launch_row_fused(int log_r, const RowParams &P, long long rows, cudaStream_t
 }
 
 // ---- column kernel dispatch -------------------------------------------------
-template <bool INV, int LB>
-int launch_col(int log_n1, const ColParams &P, cudaStream_t st) {
-  const long long total = P.nsrc * (P.npolys << COL_LOG_R);  // columns
-#define NTTB_COL(LN)                                                                   \
-  col_kernel<LN, INV, LB><<<static_cast<unsigned>(total / ColGeom<INV, LN>::SPAN), COL_THREADS, \
-                            0, st>>>(P)
+template <bool INV, int LB, int LOG_R>
+int launch_col_r(int log_n1, const ColParams &P, cudaStream_t st) {
+  const long long total = P.nsrc * (P.npolys << LOG_R);  // columns
+#define NTTB_COL(LN)                                                                          \
+  col_kernel<LN, INV, LB, LOG_R>                                                              \
+      <<<static_cast<unsigned>(total / ColGeom<INV, LN, LOG_R>::SPAN), COL_THREADS, 0, st>>>(P)
   switch (log_n1) {
     case 1: NTTB_COL(1); break;
     case 2: NTTB_COL(2); break;
     case 3: NTTB_COL(3); break;
     case 4: NTTB_COL(4); break;
     case 5: NTTB_COL(5); break;
-#undef NTTB_COL
     default: return fail(NTTMUL_EINVAL, "column count 2^%d unsupported", log_n1);
   }
+#undef NTTB_COL
   return cuda_status("col_kernel");
+}
+
+template <bool INV, int LB>
+int launch_col(int log_n1, int log_r, const ColParams &P, cudaStream_t st) {
+  switch (log_r) {
+    case 10: return launch_col_r<INV, LB, 10>(log_n1, P, st);
+    case 11: return launch_col_r<INV, LB, 11>(log_n1, P, st);
+    case 12: return launch_col_r<INV, LB, 12>(log_n1, P, st);
+    case 13: return launch_col_r<INV, LB, 13>(log_n1, P, st);
+  }
+  return fail(NTTMUL_EINVAL, "row length 2^%d unsupported", log_r);
+}
+
+// ---- radix split of n > 4096 into N1 columns x N2 = 2^log_r row length ----
+// Default 2^12 rows; nttmul_set_split picks 2^10 .. 2^13 per size (cfg5
+// sweep).  Index = log_n; 0 = default.
+int g_split[NTTMUL_MAX_LOG_N + 1] = {0};
+
+// Default split (cfg5 sweep r2, profiles/r2/cfg5_sweep_r2.jsonl): the fused
+// product keeps 4096-word rows at every size (its row kernel carries the
+// Karatsuba middle); the standalone transforms use 1024-word rows up to
+// n = 2^15 (more, smaller CTAs: -35 % single-transform latency at 2^13 /
+// 2^14, -3..-8 % per transform batched), 2048-word rows for a single 2^16
+// transform (latency) and 4096-word rows for batched 2^16 and for 2^17.
+inline int row_log(int log_n, bool xform = false, long long npolys = 0) {
+  if (log_n <= COL_LOG_R) return log_n;
+  const int r = g_split[log_n];
+  if (r) return r;
+  if (!xform) return COL_LOG_R;
+  if (log_n <= 15) return 10;
+  if (log_n == 16) return npolys <= 4 ? 11 : COL_LOG_R;
+  return COL_LOG_R;
 }
 
 // ---- small kernel -----------------------------------------------------------
@@ -186,14 +234,16 @@ int launch_cluster_t(const ClusterParams &P, long long npolys, cudaStream_t st) 
   constexpr size_t smem =
       (KIND == CL_INV ? C::G::PADN : (NP * C::G::PADN + C::N2)) * sizeof(u64);
   auto k = cluster_kernel<LOG_N1, KIND, MODE, LB>;
-  static bool ready = false;  // attributes set once per instantiation
-  if (!ready) {
-    CHECK(smem_optin(k, smem));
-    if (C::N1 > 8 &&
-        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-            cudaSuccess)
+  CHECK(smem_optin(k, smem));
+  static std::atomic<unsigned long long> ready{0};  // cluster-size opt-in done, per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ULL << (dev & 63);
+  if (C::N1 > 8 && !(ready.load() & bit)) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+        cudaSuccess)
       return cuda_status("cluster size 16 opt-in");
-    ready = true;
+    ready.fetch_or(bit);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(npolys << LOG_N1));
@@ -236,15 +286,17 @@ int launch_cluster(int log_n1, const ClusterParams &P, long long npolys, cudaStr
 // measurements (profiles/r2/NOTES.md).
 inline bool use_cluster(const int *table, int log_n, long long npolys) {
   if (log_n <= COL_LOG_R || log_n > COL_LOG_R + 4) return false;
+  if (g_split[log_n] && g_split[log_n] != COL_LOG_R) return false;  // rows of 4096 only
   const int s = table[log_n];
   if (s == NTTMUL_SCHED_THREE) return false;
   if (s == NTTMUL_SCHED_CLUSTER) return true;
-  // auto (schedule_sweep r2, profiles/r2/NOTES.md): the cluster launch wins
-  // for n = 2^13 at any batch and for single transforms up to 2^16 (one
-  // launch, no HBM round trip: -2 us); the three launches win for the
-  // larger batched products (their column passes overlap the row kernel of
-  // the other stream half; a cluster CTA waits on its own HBM phases)
-  return log_n == COL_LOG_R + 1 || (table == g_sched_xform && npolys <= 4);
+  // auto (schedule_sweep / cfg5 sweep r2, profiles/r2/NOTES.md): the
+  // cluster launch wins only for the fused product at n = 2^13 with up to
+  // ~1k limb-products (-3 %); the three launches win for larger batches and
+  // sizes (their column passes overlap the row kernel of the other stream
+  // half; a cluster CTA waits on its own HBM phases), and the 1024-word
+  // split beats the cluster for single transforms.
+  return table == g_sched_fused && log_n == COL_LOG_R + 1 && npolys <= 1024;
 }
 
 constexpr int SMALL_MAX_LOG = 9;  // n <= 2^9 -> small kernel
@@ -259,18 +311,18 @@ int run_forward(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
                   INV_NONE, FIN_PLAIN};
     return launch_small<LB>(P, NTTMUL_RED_ONE_SUB, npolys, st);
   }
-  const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
+  const int log_r = row_log(log_n, true, npolys);
   const int log_n1 = log_n - log_r;
   if constexpr (LB == 16) {  // (instantiated for the < 2^60 moduli only)
     if (use_cluster(g_sched_xform, log_n, npolys)) {
       ClusterParams P{a, a, nullptr, tw, ls, truncate ? FWD_TRUNC : FWD_FULL, INV_NONE,
                       FIN_PLAIN};
-      return launch_cluster<CL_FWD, 2, LB>(log_n1, P, npolys, st);
+      return launch_cluster<CL_FWD, 2, LB>(log_n - COL_LOG_R, P, npolys, st);
     }
   }
   if (log_n1 > 0) {
     ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, FIN_LAZY};
-    CHECK((launch_col<false, LB>(log_n1, C, st)));
+    CHECK((launch_col<false, LB>(log_n1, log_r, C, st)));
   }
   RowParams R{a, a, nullptr, tw, ls, log_n1, FIN_PLAIN, 0};
   const long long rows = npolys << log_n1;
@@ -287,12 +339,12 @@ int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
                   fin};
     return launch_small<LB>(P, NTTMUL_RED_ONE_SUB, npolys, st);
   }
-  const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
+  const int log_r = row_log(log_n, true, npolys);
   const int log_n1 = log_n - log_r;
   if constexpr (LB == 8) {  // (the inverse of every modulus < 2^61)
     if (use_cluster(g_sched_xform, log_n, npolys)) {
       ClusterParams P{a, a, nullptr, tw, ls, FWD_NONE, skip ? INV_SKIP : INV_FULL, fin};
-      return launch_cluster<CL_INV, 2, LB>(log_n1, P, npolys, st);
+      return launch_cluster<CL_INV, 2, LB>(log_n - COL_LOG_R, P, npolys, st);
     }
   }
   RowParams R{a, a, nullptr, tw, ls, log_n1, fin, 0};
@@ -301,7 +353,7 @@ int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
               : launch_row_m<FWD_NONE, false, INV_FULL, 2, LB>(log_r, R, rows, st)));
   if (log_n1 > 0) {
     ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, fin};
-    CHECK((launch_col<true, LB>(log_n1, C, st)));
+    CHECK((launch_col<true, LB>(log_n1, log_r, C, st)));
   }
   return NTTMUL_OK;
 }
@@ -323,7 +375,7 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
     SmallParams P{c, a, b, tw, ls, log_n, FWD_TRUNC, 1, INV_SKIP, FIN_SCALED_SKIP};
     return launch_small<LB>(P, MODE, npolys, st);
   }
-  const int log_r = log_n > COL_LOG_R ? COL_LOG_R : log_n;
+  const int log_r = row_log(log_n);
   const int log_n1 = log_n - log_r;
   if (log_n1 == 0) {
     if (!(phases & 2)) return NTTMUL_OK;
@@ -334,12 +386,12 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
     // constants with every modulus < 2^60 (the BASELINE bases)
     if (phases == 7 && use_cluster(g_sched_fused, log_n, npolys)) {
       ClusterParams P{c, a, b, tw, ls, FWD_TRUNC, INV_SKIP, FIN_SCALED_SKIP};
-      return launch_cluster<CL_FUSED, MODE, LB>(log_n1, P, npolys, st);
+      return launch_cluster<CL_FUSED, MODE, LB>(log_n - COL_LOG_R, P, npolys, st);
     }
   }
   if (phases & 1) {
     ColParams C{a, b, c, ws, 2, npolys, tw, ls, FIN_LAZY};
-    CHECK((launch_col<false, LB>(log_n1, C, st)));
+    CHECK((launch_col<false, LB>(log_n1, log_r, C, st)));
   }
   if (phases & 2) {
     RowParams R{c, c, ws, tw, ls, log_n1, FIN_SCALED_SKIP, 1};
@@ -347,7 +399,7 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
   }
   if (phases & 4) {
     ColParams C{c, nullptr, c, nullptr, 1, npolys, tw, ls, FIN_SCALED_SKIP};
-    CHECK((launch_col<true, LB>(log_n1, C, st)));
+    CHECK((launch_col<true, LB>(log_n1, log_r, C, st)));
   }
   return NTTMUL_OK;
 }
@@ -458,7 +510,29 @@ int check_log_n(int log_n, int min_log) {
 // constants use w1_inv when given (inverse transforms)
 int single_limb(Limb *L, u64 q, int mode, u64 mu, int s_in, int s_out,
                 int log_n, u64 w1_inv) {
-  return nttmul_limb_prepare(L, q, mode, mu, s_in, s_out, log_n, w1_inv);
+  // the scale constants cost ~2 log_n 128-bit remainders on the host: keep
+  // the last few limbs per thread (a plan's transforms repeat the same one)
+  struct Entry {
+    u64 q, mu, w1;
+    int mode, s_in, s_out, log_n;
+    Limb limb;
+  };
+  constexpr int NE = 8;
+  thread_local Entry cache[NE];
+  thread_local int used = 0, next = 0;
+  for (int i = 0; i < used; ++i) {
+    const Entry &e = cache[i];
+    if (e.q == q && e.mu == mu && e.w1 == w1_inv && e.mode == mode && e.s_in == s_in &&
+        e.s_out == s_out && e.log_n == log_n) {
+      *L = e.limb;
+      return NTTMUL_OK;
+    }
+  }
+  CHECK(nttmul_limb_prepare(L, q, mode, mu, s_in, s_out, log_n, w1_inv));
+  cache[next] = Entry{q, mu, w1_inv, mode, s_in, s_out, log_n, *L};
+  next = (next + 1) % NE;
+  if (used < NE) ++used;
+  return NTTMUL_OK;
 }
 
 TwSet one_table(const u64 *pairs) {
@@ -737,6 +811,14 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
            reinterpret_cast<const ulonglong2 *>(inv_pairs), stride};
   return run_polymul(mode, lbx, c, a, b, workspace, tw, ls, log_n,
                      batch * num_limbs, phases, S(stream));
+}
+
+int nttmul_set_split(int log_n, int log_r) {
+  if (log_n <= COL_LOG_R || log_n > NTTMUL_MAX_LOG_N ||
+      (log_r != 0 && (log_r < 10 || log_r > 13 || log_n - log_r < 1 || log_n - log_r > 5)))
+    return fail(NTTMUL_EINVAL, "set_split(%d, %d)", log_n, log_r);
+  g_split[log_n] = log_r;
+  return NTTMUL_OK;
 }
 
 int nttmul_set_schedule(int which, int log_n, int schedule) {

@@ -438,9 +438,15 @@ __device__ __forceinline__ void sbar_wait(u64 *bar, unsigned parity) {
       : "memory");
 }
 
+// resident CTAs per SM of a row kernel (512-thread rows: 2; the 1024-thread
+// rows of the 8192-word split: 1)
+template <int LOG_R, bool MID>
+constexpr int row_minb() {
+  return RowGeom<LOG_R>::T >= 1024 ? 1 : (MID ? NTTB_ROW_MINB_FUSED : NTTB_ROW_MINB);
+}
+
 template <int LOG_R, int FWD, bool MID, int INV, int MODE, int LB>
-__global__ void __launch_bounds__(RowGeom<LOG_R>::T,
-                                  MID ? NTTB_ROW_MINB_FUSED : NTTB_ROW_MINB)
+__global__ void __launch_bounds__(RowGeom<LOG_R>::T, (row_minb<LOG_R, MID>()))
     row_kernel(const RowParams P) {
   using G = RowGeom<LOG_R>;
   constexpr int NP = MID ? 2 : 1;
@@ -603,20 +609,23 @@ __device__ __forceinline__ void col_inv_stages(u64 (&x)[1][1 << LOG_N1], const u
 // LOG_N1 column stages on them in registers; the stages' twiddles tw[1 ..
 // N1) are uniform across the CTA.  Short columns (N1 <= 8) take several per
 // thread so that 16 loads per thread are in flight.
-template <bool INV, int LOG_N1>
+// LOG_R: the row length 2^LOG_R of the split (= the number of columns of a
+// polynomial); COL_LOG_R = 12 unless nttmul_set_split chose another.
+template <bool INV, int LOG_N1, int LOG_R = COL_LOG_R>
 struct ColGeom {
   // 32-word columns (n = 2^17) need the register budget of 2 CTAs/SM
   static constexpr int MINB = LOG_N1 >= 5 ? 2 : (INV ? NTTB_COL_MINB_INV : NTTB_COL_MINB);
-  static constexpr int COLS = LOG_N1 >= 4 ? 1 : (16 >> LOG_N1);
+  static constexpr int WANT = LOG_N1 >= 4 ? 1 : (16 >> LOG_N1);
+  static constexpr int COLS = COL_THREADS * WANT <= (1 << LOG_R) ? WANT : (1 << LOG_R) / COL_THREADS;
   static constexpr int SPAN = COL_THREADS * COLS;  // columns per CTA
 };
 
-template <int LOG_N1, bool INV, int LB>
+template <int LOG_N1, bool INV, int LB, int LOG_R = COL_LOG_R>
 __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col_kernel(const ColParams P) {
   constexpr int N1 = 1 << LOG_N1;
-  using CG = ColGeom<INV, LOG_N1>;
+  using CG = ColGeom<INV, LOG_N1, LOG_R>;
   constexpr int COLS = CG::COLS;
-  const long long cols = P.npolys << COL_LOG_R;  // columns per source
+  const long long cols = P.npolys << LOG_R;  // columns per source
   // a CTA's SPAN columns lie in one polynomial of one source (4096 columns
   // per polynomial), so source, polynomial and limb are CTA-uniform: derive
   // them from blockIdx only
@@ -624,9 +633,8 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
   if (cta0 >= cols * P.nsrc) return;
   const int which = cta0 >= cols ? 1 : 0;
   const long long first = cta0 - (which ? cols : 0);
-  const long long poly = first >> COL_LOG_R;
-  const long long base = (poly << (COL_LOG_R + LOG_N1)) +
-                         ((first + threadIdx.x) & ((1 << COL_LOG_R) - 1));
+  const long long poly = first >> LOG_R;
+  const long long base = (poly << (LOG_R + LOG_N1)) + ((first + threadIdx.x) & ((1 << LOG_R) - 1));
   int limb;
   const Limb &L = *limb_ptr(P.limbs, poly, limb);
   const Mod M = mod_for_stages<LB>(L.q);
@@ -643,7 +651,7 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
   for (int k = 0; k < COLS; ++k)
 #pragma unroll
     for (int e = 0; e < N1; ++e)
-      x[k][0][e] = src[(static_cast<long long>(e) << COL_LOG_R) + k * COL_THREADS];
+      x[k][0][e] = src[(static_cast<long long>(e) << LOG_R) + k * COL_THREADS];
   __shared__ ulonglong2 stw[N1];
   const ulonglong2 *tg = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
   if (threadIdx.x < N1) stw[threadIdx.x] = tg[threadIdx.x];
@@ -656,7 +664,7 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
       col_inv_stages<LB, LOG_N1>(x[k], stw, L, M, P.fin);
 #pragma unroll
     for (int e = 0; e < N1; ++e)
-      dst[(static_cast<long long>(e) << COL_LOG_R) + k * COL_THREADS] = x[k][0][e];
+      dst[(static_cast<long long>(e) << LOG_R) + k * COL_THREADS] = x[k][0][e];
   }
 }
 

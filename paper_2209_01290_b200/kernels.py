@@ -205,8 +205,9 @@ def ntt_ct(a, tw, q, mode, mu, s_in, s_out, truncate, counts=None):
     _lib.call("nttmul_ntt_ct", op.dev.data_ptr(), pairs.data_ptr(), int(q), int(mode), int(mu),
               int(s_in), int(s_out), int(bool(truncate)), log_n, batch, _device.stream_ptr())
     op.writeback()
-    mul, _, groups = _fwd_counts(n, bool(truncate))
-    _add_counts(counts, (batch * mul, 2 * batch * mul, 0, batch * groups, 0))
+    if counts is not None:
+        mul, _, groups = _fwd_counts(n, bool(truncate))
+        _add_counts(counts, (batch * mul, 2 * batch * mul, 0, batch * groups, 0))
 
 
 def intt_gs(a, tw, q, half_q, mode, mu, s_in, s_out, scaled, skip_first, counts=None):
@@ -222,9 +223,10 @@ def intt_gs(a, tw, q, half_q, mode, mu, s_in, s_out, scaled, skip_first, counts=
               int(mode), int(mu), int(s_in), int(s_out), int(bool(scaled)),
               int(bool(skip_first)), log_n, batch, w1, _device.stream_ptr())
     op.writeback()
-    mul, _, groups = _inv_counts(n, bool(skip_first))
-    _add_counts(counts, (batch * mul, 2 * batch * mul, 2 * batch * mul if scaled else 0,
-                         batch * groups, 0))
+    if counts is not None:
+        mul, _, groups = _inv_counts(n, bool(skip_first))
+        _add_counts(counts, (batch * mul, 2 * batch * mul, 2 * batch * mul if scaled else 0,
+                             batch * groups, 0))
 
 
 def fused_middle(ah, bh, ch, tw, q, mode, mu, s_in, s_out, counts=None):

@@ -109,3 +109,50 @@ def test_schedule_knob_rejects_bad_arguments():
     for args in ((2, 14, 1), (0, 12, 1), (0, 17, 1), (0, 14, 3)):
         with pytest.raises(nt._lib.NttmulError):
             lib.call("nttmul_set_schedule", *args)
+
+
+# ---- radix splits (nttmul_set_split, BASELINE cfg5) ------------------------
+
+@contextlib.contextmanager
+def split(log_n, log_r):
+    lib.call("nttmul_set_split", log_n, log_r)
+    try:
+        yield
+    finally:
+        lib.call("nttmul_set_split", log_n, 0)
+
+
+@pytest.mark.parametrize("log_n,log_r", [(13, 10), (13, 11), (14, 10), (14, 13), (15, 11),
+                                         (15, 13), (16, 11), (16, 13), (17, 13)])
+def test_radix_splits_bit_exact(log_n, log_r):
+    n = 1 << log_n
+    basis = nt.RnsBasis.build(n, 60, 2, seed=0)
+    A = np.stack([np.stack([rand(q, n, 5 * b + l) for l, q in enumerate(basis.primes)])
+                  for b in range(2)])
+    Bm = np.stack([np.stack([rand(q, n, 77 + 5 * b + l) for l, q in enumerate(basis.primes)])
+                   for b in range(2)])
+    with split(log_n, log_r), schedule(0, log_n, lib.SCHED_THREE) if log_n <= 16 else \
+            contextlib.nullcontext():
+        got = nt.polymul_rns_batch(dev(A), dev(Bm), basis).cpu().numpy()
+    want = oracle.polymul_rns(A[:1], Bm[:1], basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(got[:1], want)
+    plan = basis.plans[0]
+    f, v = oracle.twiddles(plan.q, plan.psi, log_n)
+    rows = A[:, 0].copy()
+    want = rows.copy()
+    for w in want:
+        oracle.ntt_ct(w, f, *plan.red_args, False)
+    x = dev(rows)
+    with split(log_n, log_r), schedule(1, log_n, lib.SCHED_THREE) if log_n <= 16 else \
+            contextlib.nullcontext():
+        nt.kernels.ntt_ct(x, plan.tw_fwd, *plan.red_args, False, None)
+        assert np.array_equal(x.cpu().numpy(), want)
+        nt.kernels.intt_gs(x, plan.tw_inv, plan.q, (plan.q + 1) // 2, *plan.red_args[1:],
+                           True, False, None)
+    assert np.array_equal(x.cpu().numpy(), rows)
+
+
+def test_split_knob_rejects_bad_arguments():
+    for args in ((12, 10), (14, 9), (14, 14), (17, 11), (18, 13)):
+        with pytest.raises(nt._lib.NttmulError):
+            lib.call("nttmul_set_split", *args)
