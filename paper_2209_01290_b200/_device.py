@@ -19,9 +19,19 @@ def require_cuda() -> None:
                            "there is no CPU fallback")
 
 
-def device() -> torch.device:
+_get_device = getattr(torch._C, "_cuda_getDevice", None)
+
+
+def index() -> int:
+    """Current CUDA device index (the raw getter: no lazy-init bookkeeping)."""
+    if _get_device is not None and torch.cuda.is_initialized():
+        return _get_device()
     require_cuda()
-    return torch.device("cuda", torch.cuda.current_device())
+    return torch.cuda.current_device()
+
+
+def device() -> torch.device:
+    return torch.device("cuda", index())
 
 
 _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
@@ -31,7 +41,7 @@ def stream_ptr() -> int:
     """cudaStream_t of torch's current stream (the launch stream) - the raw
     handle without building a torch.cuda.Stream object (a few us per call)."""
     if _raw_stream is not None:
-        return _raw_stream(torch.cuda.current_device())
+        return _raw_stream(index())
     return torch.cuda.current_stream().cuda_stream
 
 

@@ -56,6 +56,14 @@ int check_dev(const void *p, size_t align, const char *name) {
   if (!p) return fail(NTTMUL_EPTR, "%s is NULL", name);
   if (reinterpret_cast<uintptr_t>(p) % align)
     return fail(NTTMUL_EALIGN, "%s not %zu-byte aligned", name, align);
+  // cudaPointerGetAttributes costs ~1 us of host time per call: remember
+  // the last few device pointers this thread validated (device addresses
+  // never turn into host addresses under UVA; a freed one passed again is
+  // the caller's use-after-free, which the reference does not check either)
+  thread_local const void *seen[16] = {};
+  thread_local int next = 0;
+  for (const void *s : seen)
+    if (s == p) return NTTMUL_OK;
   cudaPointerAttributes at;
   const cudaError_t e = cudaPointerGetAttributes(&at, p);
   if (e != cudaSuccess) {
@@ -64,6 +72,8 @@ int check_dev(const void *p, size_t align, const char *name) {
   }
   if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
     return fail(NTTMUL_EPTR, "%s is not device memory", name);
+  seen[next] = p;
+  next = (next + 1) % 16;
   return NTTMUL_OK;
 }
 

@@ -62,7 +62,7 @@ def _evict(key) -> None:
 
 
 def _remember(tw, q: int, entry) -> None:
-    key = (id(tw), q, torch.cuda.current_device())
+    key = (id(tw), q, _device.index())
     if key not in _PAIRS:
         while len(_PAIRS) >= _PAIRS_MAX:
             _PAIRS.pop(next(iter(_PAIRS)))
@@ -77,7 +77,7 @@ def register_pairs(tw: torch.Tensor, pairs: torch.Tensor, q: int, w1: int) -> No
 
 
 def _lookup(tw, q: int):
-    hit = _PAIRS.get((id(tw), q, torch.cuda.current_device()))
+    hit = _PAIRS.get((id(tw), q, _device.index()))
     if hit is None:
         return None
     version, pref, w1, host_copy = hit

@@ -141,10 +141,10 @@ class NttPlan:
 
     # -- device tables (one set per CUDA device) ---------------------------
     def _tables(self) -> tuple:
-        dev = _device.device()
-        t = self._dev_tables.get(dev.index)
+        t = self._dev_tables.get(_device.index())
         if t is not None:
             return t
+        dev = _device.device()
         st = _device.stream_ptr()
         n = self.n
         fwd_pairs = torch.empty((n, 2), dtype=_device.U64, device=dev)
