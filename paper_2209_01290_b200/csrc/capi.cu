@@ -113,6 +113,31 @@ int smem_optin(K kernel, size_t bytes) {
   return NTTMUL_OK;
 }
 
+// ---- launch with programmatic dependent launch ------------------------------
+// The column / row kernels of a transform are launched with programmatic
+// stream serialization: each may be scheduled while its predecessor's last
+// wave still runs and waits (griddepcontrol.wait) for its results, so the
+// launch gaps between the three launches of a product disappear
+// (ntt_kernels.cuh pdl_wait).  NTTB_NO_PDL=1 (environment) launches plainly.
+template <class K, class Arg>
+int launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const Arg &arg) {
+  static const bool off = std::getenv("NTTB_NO_PDL") != nullptr;
+  if (grid.x == 0) return NTTMUL_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, arg);
+  if (e != cudaSuccess) return fail(NTTMUL_ELAUNCH, "launch: %s", cudaGetErrorString(e));
+  return NTTMUL_OK;
+}
+
 // ---- row kernel dispatch ---------------------------------------------------
 #ifndef NTTB_ROW_PF
 #define NTTB_ROW_PF 1  // L2 prefetch of the rows one resident wave ahead
@@ -141,7 +166,7 @@ int launch_row_t(const RowParams &P, long long rows, cudaStream_t st) {
   RowParams Q = P;
   Q.nrows = rows;
   Q.pf_dist = NTTB_ROW_PF ? slots : 0;
-  k<<<static_cast<unsigned>(rows), RowGeom<LOG_R>::T, smem, st>>>(Q);
+  CHECK(launch_pdl(k, dim3(static_cast<unsigned>(rows)), dim3(RowGeom<LOG_R>::T), smem, st, Q));
   return cuda_status("row_kernel");
 }
 
@@ -166,9 +191,10 @@ int launch_row_fused(int log_r, const RowParams &P, long long rows, cudaStream_t
 template <bool INV, int LB, int LOG_R>
 int launch_col_r(int log_n1, const ColParams &P, cudaStream_t st) {
   const long long total = P.nsrc * (P.npolys << LOG_R);  // columns
-#define NTTB_COL(LN)                                                                          \
-  col_kernel<LN, INV, LB, LOG_R>                                                              \
-      <<<static_cast<unsigned>(total / ColGeom<INV, LN, LOG_R>::SPAN), COL_THREADS, 0, st>>>(P)
+#define NTTB_COL(LN)                                                                 \
+  CHECK(launch_pdl(col_kernel<LN, INV, LB, LOG_R>,                                     \
+                   dim3(static_cast<unsigned>(total / ColGeom<INV, LN, LOG_R>::SPAN)), \
+                   dim3(COL_THREADS), 0, st, P))
   switch (log_n1) {
     case 1: NTTB_COL(1); break;
     case 2: NTTB_COL(2); break;

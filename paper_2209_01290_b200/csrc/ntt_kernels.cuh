@@ -169,6 +169,18 @@ __device__ __forceinline__ void discard_line(const void *line) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
 }
 
+// Programmatic dependent launch (the column / row / column launches of one
+// transform): a kernel signals at its start that its dependents may be
+// scheduled (their CTAs then take the SM slots its last wave leaves free)
+// and waits for its predecessor's results before touching global data.
+// Without the launch attribute both are no-ops / return at once.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // bulk prefetch of [p, p + bytes) into L2 (no register or smem cost)
 __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -461,6 +473,8 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T, (row_minb<LOG_R, MID>()))
   const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
   const u64 rowbase = (1ULL << P.log_n1) + r;  // (N1 + r): group index base
   const long long off = row * G::N2;
+  pdl_launch_dependents();
+  pdl_wait();
   // Rows are dispatched in order, so the CTA that takes row + pf_dist (one
   // resident wave later) starts about when this one ends: pull its inputs
   // into L2 now so its first pass does not wait on HBM latency.
@@ -640,6 +654,8 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
   const Mod M = mod_for_stages<LB>(L.q);
   const u64 *__restrict__ src = (which ? P.src1 : P.src0) + base;
   u64 *__restrict__ dst = (which ? P.dst1 : P.dst0) + base;
+  pdl_launch_dependents();
+  pdl_wait();
   // The column loads go out first; the N1 - 1 twiddles (the same for the
   // whole CTA) are staged in shared memory behind them, so the butterflies
   // read them just in time (LDS broadcast) instead of the compiler hoisting
