@@ -565,8 +565,9 @@ def run_e2e(nt, basis, A_h, B_h, args, world, stream, C_dev, cts_per_step, allre
                     "(chunked H2D / fused kernels / D2H on 3 streams) -> pinned host",
             "numpy_unpinned": {"value": round(cts_per_step * nsteps / (ms_np / 1e3), 2),
                                "steps": nsteps,
-                               "path": "polymul_rns_batch(numpy ndarrays): pin_memory staging "
-                                       "copy of a and b, then the same streamed call"}}
+                               "path": "polymul_rns_batch(numpy ndarrays): chunks staged "
+                                       "through two pinned slots by host threads, overlapped "
+                                       "with the streamed GPU chunks; numpy result"}}
 
 
 def modmul_roof(nt, basis, stream):
