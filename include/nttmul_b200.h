@@ -247,7 +247,8 @@ int nttmul_polymul_fused_rns_host(uint64_t *c_host, const uint64_t *a_host,
                                   void *stream);
 
 /*
- * Schedule of the transforms of n = 2^13 .. 2^16 (process-wide, per size):
+ * Schedule of the transforms of n = 2^13 .. 2^17 (process-wide, per size; the
+ * cluster schedule covers 2^13 .. 2^16):
  * which = 0 selects the fused product (nttmul_polymul_fused_rns*), 1 the
  * standalone ntt_ct / intt_gs.  NTTMUL_SCHED_THREE runs the column / row /
  * column launches through HBM; NTTMUL_SCHED_CLUSTER one launch of one
@@ -268,6 +269,10 @@ int nttmul_set_split(int log_n, int log_r);
 #define NTTMUL_SCHED_AUTO 0
 #define NTTMUL_SCHED_THREE 1
 #define NTTMUL_SCHED_CLUSTER 2
+/* standalone transforms only: the column stages as strided passes of <= 3
+ * stages (more, shorter CTAs) before rows of 1024 words - the latency
+ * schedule of a single large transform */
+#define NTTMUL_SCHED_PASSES 3
 int nttmul_set_schedule(int which, int log_n, int schedule);
 
 /* ---- RNS decomposition / CRT reconstruction (rns.py:82-108) ------------- */

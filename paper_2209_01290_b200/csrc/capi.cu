@@ -218,6 +218,30 @@ int launch_col(int log_n1, int log_r, const ColParams &P, cudaStream_t st) {
   return fail(NTTMUL_EINVAL, "row length 2^%d unsupported", log_r);
 }
 
+// ---- strided column passes (latency schedule) --------------------------------
+template <bool INV, int LB>
+int launch_pass(int r, const PassParams &P, cudaStream_t st) {
+  const long long units = P.npolys << (P.log_n - r);
+  const dim3 grid(static_cast<unsigned>((units + PASS_THREADS - 1) / PASS_THREADS));
+  switch (r) {
+    case 1: CHECK(launch_pdl(pass_kernel<1, INV, LB>, grid, dim3(PASS_THREADS), 0, st, P)); break;
+    case 2: CHECK(launch_pdl(pass_kernel<2, INV, LB>, grid, dim3(PASS_THREADS), 0, st, P)); break;
+    case 3: CHECK(launch_pdl(pass_kernel<3, INV, LB>, grid, dim3(PASS_THREADS), 0, st, P)); break;
+    default: return fail(NTTMUL_EINVAL, "pass of %d stages", r);
+  }
+  return cuda_status("pass_kernel");
+}
+
+// The column stages [0, c) of the latency schedule as passes of <= 3 stages
+// (balanced: 4 -> 2 + 2, 5 -> 3 + 2, 6 -> 3 + 3, 7 -> 3 + 2 + 2).
+inline int pass_plan(int c, int *r) {
+  const int np = (c + 2) / 3;
+  for (int i = 0; i < np; ++i) r[i] = c / np + (i < c % np ? 1 : 0);
+  return np;
+}
+
+constexpr int LAT_LOG_R = 10;  // row length of the latency schedule
+
 // ---- radix split of n > 4096 into N1 columns x N2 = 2^log_r row length ----
 // Default 2^12 rows; nttmul_set_split picks 2^10 .. 2^13 per size (cfg5
 // sweep).  Index = log_n; 0 = default.
@@ -320,6 +344,19 @@ int launch_cluster(int log_n1, const ClusterParams &P, long long npolys, cudaStr
 
 // Default schedule (NTTMUL_SCHED_AUTO) per size, from the round-2
 // measurements (profiles/r2/NOTES.md).
+// Latency schedule of the standalone transforms: strided passes + rows of
+// 2^10.  Auto (latency_sweep r2, profiles/r2/latency_r2.jsonl): a single
+// forward transform of 2^13, 2^15 or 2^16 words and a single inverse of
+// 2^13 .. 2^17 words (2^16: ntt 9.9 -> 7.9 us, intt 11.7 -> 8.6 us); batches
+// keep the column kernel (one HBM round trip for all column stages).
+inline bool use_passes(int log_n, long long npolys, bool inverse) {
+  if (log_n <= COL_LOG_R || g_split[log_n]) return false;
+  const int s = g_sched_xform[log_n];
+  if (s == NTTMUL_SCHED_PASSES) return true;
+  if (s != NTTMUL_SCHED_AUTO || npolys != 1) return false;
+  return inverse || log_n == 13 || log_n == 15 || log_n == 16;
+}
+
 inline bool use_cluster(const int *table, int log_n, long long npolys) {
   if (log_n <= COL_LOG_R || log_n > COL_LOG_R + 4) return false;
   if (g_split[log_n] && g_split[log_n] != COL_LOG_R) return false;  // rows of 4096 only
@@ -356,6 +393,18 @@ int run_forward(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
       return launch_cluster<CL_FWD, 2, LB>(log_n - COL_LOG_R, P, npolys, st);
     }
   }
+  if (use_passes(log_n, npolys, false)) {
+    const int c = log_n - LAT_LOG_R;
+    int r[4];
+    const int np = pass_plan(c, r);
+    for (int i = 0, s0 = 0; i < np; s0 += r[i], ++i) {
+      PassParams Q{a, tw, ls, log_n, s0, npolys, FIN_LAZY};
+      CHECK((launch_pass<false, LB>(r[i], Q, st)));
+    }
+    RowParams R{a, a, nullptr, tw, ls, c, FIN_PLAIN, 0};
+    return truncate ? launch_row_m<FWD_TRUNC, false, INV_NONE, 2, LB>(LAT_LOG_R, R, npolys << c, st)
+                    : launch_row_m<FWD_FULL, false, INV_NONE, 2, LB>(LAT_LOG_R, R, npolys << c, st);
+  }
   if (log_n1 > 0) {
     ColParams C{a, nullptr, a, nullptr, 1, npolys, tw, ls, FIN_LAZY};
     CHECK((launch_col<false, LB>(log_n1, log_r, C, st)));
@@ -382,6 +431,21 @@ int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
       ClusterParams P{a, a, nullptr, tw, ls, FWD_NONE, skip ? INV_SKIP : INV_FULL, fin};
       return launch_cluster<CL_INV, 2, LB>(log_n - COL_LOG_R, P, npolys, st);
     }
+  }
+  if (use_passes(log_n, npolys, true)) {
+    const int c = log_n - LAT_LOG_R;
+    RowParams R{a, a, nullptr, tw, ls, c, fin, 0};
+    CHECK((skip ? launch_row_m<FWD_NONE, false, INV_SKIP, 2, LB>(LAT_LOG_R, R, npolys << c, st)
+                : launch_row_m<FWD_NONE, false, INV_FULL, 2, LB>(LAT_LOG_R, R, npolys << c, st)));
+    int r[4];
+    const int np = pass_plan(c, r);
+    int s0 = c;
+    for (int i = np - 1; i >= 0; --i) {
+      s0 -= r[i];
+      PassParams Q{a, tw, ls, log_n, s0, npolys, s0 == 0 ? fin : FIN_LAZY};
+      CHECK((launch_pass<true, LB>(r[i], Q, st)));
+    }
+    return NTTMUL_OK;
   }
   RowParams R{a, a, nullptr, tw, ls, log_n1, fin, 0};
   const long long rows = npolys << log_n1;
@@ -858,8 +922,10 @@ int nttmul_set_split(int log_n, int log_r) {
 }
 
 int nttmul_set_schedule(int which, int log_n, int schedule) {
-  if (which < 0 || which > 1 || log_n < COL_LOG_R + 1 || log_n > COL_LOG_R + 4 ||
-      schedule < NTTMUL_SCHED_AUTO || schedule > NTTMUL_SCHED_CLUSTER)
+  if (which < 0 || which > 1 || log_n < COL_LOG_R + 1 || log_n > NTTMUL_MAX_LOG_N ||
+      schedule < NTTMUL_SCHED_AUTO || schedule > NTTMUL_SCHED_PASSES ||
+      (schedule == NTTMUL_SCHED_PASSES && which == 0) ||
+      (schedule == NTTMUL_SCHED_CLUSTER && log_n > COL_LOG_R + 4))
     return fail(NTTMUL_EINVAL, "set_schedule(%d, %d, %d)", which, log_n, schedule);
   (which == 0 ? g_sched_fused : g_sched_xform)[log_n] = schedule;
   return NTTMUL_OK;

@@ -685,6 +685,60 @@ __global__ void __launch_bounds__(COL_THREADS, (ColGeom<INV, LOG_N1>::MINB)) col
 }
 
 // ---------------------------------------------------------------------------
+// STRIDED PASS kernel: R consecutive column stages [S0, S0 + R) of one
+// transform over global memory, one 2^R-element unit per thread (elements
+// k_last = n >> (S0 + R) apart, consecutive threads on consecutive j, so
+// every load and store is coalesced).  The latency schedule of a single
+// large transform chains a few of these (3 stages each) before a row
+// kernel of 1024-word rows: more, shorter CTAs than one column kernel whose
+// threads each carry a whole 16- or 32-deep column.
+
+struct PassParams {
+  u64 *a;
+  TwSet tw;
+  LimbSet limbs;
+  int log_n;
+  int s0;
+  long long npolys;
+  int fin;  // inverse pass with s0 == 0: FinalMode of the global last stage
+};
+
+constexpr int PASS_THREADS = 128;
+
+template <int R, bool INV, int LB>
+__global__ void __launch_bounds__(PASS_THREADS) pass_kernel(const PassParams P) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int log_u = P.log_n - R;              // units per polynomial = 2^log_u
+  const int log_k = P.log_n - P.s0 - R;       // log2(k_last)
+  const long long uid = blockIdx.x * static_cast<long long>(PASS_THREADS) + threadIdx.x;
+  if (uid >= (P.npolys << log_u)) return;
+  const long long poly = uid >> log_u;
+  const long long u = uid & ((1LL << log_u) - 1);
+  const long long grp = u >> log_k;
+  const long long j = u & ((1LL << log_k) - 1);
+  int limb;
+  const Limb &L = *limb_ptr(P.limbs, poly, limb);
+  const Mod M = mod_for_stages<LB>(L.q);
+  const ulonglong2 *tw = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
+  u64 *base = P.a + (poly << P.log_n) + (grp << (log_k + R)) + j;
+  u64 x[1][1 << R];
+#pragma unroll
+  for (int e = 0; e < (1 << R); ++e) x[0][e] = base[static_cast<long long>(e) << log_k];
+  const u64 B0 = (1ULL << P.s0) + static_cast<u64>(grp);
+  if (!INV) {
+    fwd_radix<LB, R, R, 1>(x, B0, tw, M);  // starts with a reducing stage
+  } else if (P.s0 == 0) {
+    inv_radix<LB, R, R, 1, 1>(x, B0, tw, M);
+    inv_stage0<LB, R, 1>(x, B0, tw, L, M, P.fin);
+  } else {
+    inv_radix<LB, R, R, 0, 1>(x, B0, tw, M);
+  }
+#pragma unroll
+  for (int e = 0; e < (1 << R); ++e) base[static_cast<long long>(e) << log_k] = x[0][e];
+}
+
+// ---------------------------------------------------------------------------
 // SMALL kernel: n <= 2^12, one CTA per polynomial (per pair when fused);
 // stage loop over shared memory.  Used for n < 2^10 (the reference's unit
 // test sizes); also a schedule-independent cross-check of the row kernel.

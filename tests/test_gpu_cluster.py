@@ -106,7 +106,7 @@ def test_cluster_standalone_transforms(log_n):
 
 
 def test_schedule_knob_rejects_bad_arguments():
-    for args in ((2, 14, 1), (0, 12, 1), (0, 17, 1), (0, 14, 3)):
+    for args in ((2, 14, 1), (0, 12, 1), (0, 17, 2), (0, 14, 3), (1, 18, 1), (1, 17, 2)):
         with pytest.raises(nt._lib.NttmulError):
             lib.call("nttmul_set_schedule", *args)
 
@@ -156,3 +156,32 @@ def test_split_knob_rejects_bad_arguments():
     for args in ((12, 10), (14, 9), (14, 14), (17, 11), (18, 13)):
         with pytest.raises(nt._lib.NttmulError):
             lib.call("nttmul_set_split", *args)
+
+
+@pytest.mark.parametrize("log_n", [13, 14, 15, 16, 17])
+@pytest.mark.parametrize("batch", [1, 3])
+def test_latency_pass_schedule_bit_exact(log_n, batch):
+    """Strided column passes of <= 3 stages + 1024-word rows
+    (NTTMUL_SCHED_PASSES) for ntt_ct (full / truncated) and intt_gs (scaled
+    full / skip_first / plain)."""
+    n = 1 << log_n
+    plan = nt.build_plan(n, bits=60, seed=2)
+    f, v = oracle.twiddles(plan.q, plan.psi, log_n)
+    rows = np.stack([rand(plan.q, n, 31 + i) for i in range(batch)])
+    args = plan.red_args
+    half_q = (plan.q + 1) // 2
+    with schedule(1, log_n, lib.SCHED_PASSES):
+        for truncate in (False, True):
+            want = rows.copy()
+            for w in want:
+                oracle.ntt_ct(w, f, *args, truncate)
+            x = dev(rows)
+            nt.kernels.ntt_ct(x, plan.tw_fwd, *args, truncate, None)
+            assert np.array_equal(x.cpu().numpy(), want), f"ntt_ct truncate={truncate}"
+        for scaled, skip in ((True, False), (True, True), (False, False)):
+            want = rows.copy()
+            for w in want:
+                oracle.intt_gs(w, v, plan.q, half_q, *args[1:], scaled, skip)
+            x = dev(rows)
+            nt.kernels.intt_gs(x, plan.tw_inv, plan.q, half_q, *args[1:], scaled, skip, None)
+            assert np.array_equal(x.cpu().numpy(), want), f"intt scaled={scaled} skip={skip}"
