@@ -693,9 +693,26 @@ def crt_rates(nt, basis, batch):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps, out
 
-    dec_ms, res = timed(lambda: nt.crt_decompose(words, basis))
-    rec_ms, back = timed(lambda: nt.crt_reconstruct(res, basis))
+    # the C-ABI calls on preallocated buffers (the Python wrappers allocate
+    # their outputs; kernel time only here), checked by a round trip
+    t = nt.rns._crt_tables(basis)
+    res = torch.empty((batch, L, n), dtype=torch.uint64, device="cuda")
+    back = torch.empty_like(words)
+    sp = stream.cuda_stream
+
+    def dec():
+        nt._lib.call("nttmul_crt_decompose", res.data_ptr(), words.data_ptr(),
+                     t["primes"].data_ptr(), t["dec"].data_ptr(), L, W, batch, n, sp)
+
+    def rec():
+        nt._lib.call("nttmul_crt_reconstruct", back.data_ptr(), res.data_ptr(),
+                     t["primes"].data_ptr(), t["inv"].data_ptr(), t["m"].data_ptr(),
+                     t["q"].data_ptr(), t["recip"].data_ptr(), L, W, batch, n, sp)
+
+    dec_ms, _ = timed(dec)
+    rec_ms, _ = timed(rec)
     assert torch.equal(back, words), "CRT round trip"
+    assert torch.equal(nt.crt_decompose(words, basis), res), "CRT wrapper"
     nbytes = batch * n * (W + L) * 8
     return {"words_per_coeff": W, "decompose_ms_per_poly": round(dec_ms / batch, 4),
             "reconstruct_ms_per_poly": round(rec_ms / batch, 4),

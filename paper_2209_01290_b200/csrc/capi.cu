@@ -113,6 +113,24 @@ int smem_optin(K kernel, size_t bytes) {
   return NTTMUL_OK;
 }
 
+// The largest shared-memory carveout for kernels whose residency is set by
+// their shared memory (the CRT kernels: 26 KB per 128-thread block).  Left
+// to the driver, the carveout - and with it the blocks per SM - varied from
+// run to run (crt_decompose 0.031 .. 0.088 ms per polynomial).
+template <class K>
+int prefer_smem(K kernel) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ULL << (dev & 63);
+  if (done.load() & bit) return NTTMUL_OK;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+    return cuda_status("shared memory carveout");
+  done.fetch_or(bit);
+  return NTTMUL_OK;
+}
+
 // ---- launch with programmatic dependent launch ------------------------------
 // The column / row kernels of a transform are launched with programmatic
 // stream serialization: each may be scheduled while its predecessor's last
@@ -1104,6 +1122,7 @@ int nttmul_crt_decompose(uint64_t *res, const uint64_t *words, const uint64_t *p
   if (smem > 200 * 1024) return fail(NTTMUL_EINVAL, "crt_decompose: L=%d W=%d too large",
                                      num_limbs, num_words);
   CHECK(smem_optin(crt_decompose_kernel, smem));
+  CHECK(prefer_smem(crt_decompose_kernel));
   crt_decompose_kernel<<<grid, CRT_THREADS, smem, S(stream)>>>(res, words, primes, pw, num_limbs,
                                                                num_words, n, total);
   return cuda_status("crt_decompose_kernel");
@@ -1129,6 +1148,7 @@ int nttmul_crt_reconstruct(uint64_t *words, const uint64_t *res, const uint64_t 
   const size_t smem =
       static_cast<size_t>(CRT_THREADS) * (crt_stride(num_words) + num_limbs) * sizeof(u64);
   CHECK(smem_optin(crt_reconstruct_kernel, smem));
+  CHECK(prefer_smem(crt_reconstruct_kernel));
   crt_reconstruct_kernel<<<grid, CRT_THREADS, smem, S(stream)>>>(
       words, res, primes, iv, m_words, q_words, q_recip, num_limbs, num_words, n, total);
   return cuda_status("crt_reconstruct_kernel");
