@@ -185,3 +185,24 @@ def test_latency_pass_schedule_bit_exact(log_n, batch):
             x = dev(rows)
             nt.kernels.intt_gs(x, plan.tw_inv, plan.q, half_q, *args[1:], scaled, skip, None)
             assert np.array_equal(x.cpu().numpy(), want), f"intt scaled={scaled} skip={skip}"
+
+
+@pytest.mark.parametrize("log_n,batch", [(13, 131), (16, 128)])
+def test_batched_transforms_large_batches(log_n, batch):
+    """Large batches of standalone transforms (odd counts, > one wave of
+    row CTAs): every row equals the oracle's transform and round-trips."""
+    n = 1 << log_n
+    plan = nt.build_plan(n, bits=60, seed=4)
+    f, v = oracle.twiddles(plan.q, plan.psi, log_n)
+    base = np.stack([rand(plan.q, n, 900 + i) for i in range(3)])
+    rows = base[np.arange(batch) % 3]
+    want = base.copy()
+    for w in want:
+        oracle.ntt_ct(w, f, *plan.red_args, False)
+    x = dev(rows)
+    nt.kernels.ntt_ct(x, plan.tw_fwd, *plan.red_args, False, None)
+    got = x.cpu().numpy()
+    assert np.array_equal(got, want[np.arange(batch) % 3])
+    nt.kernels.intt_gs(x, plan.tw_inv, plan.q, (plan.q + 1) // 2, *plan.red_args[1:], True,
+                       False, None)
+    assert np.array_equal(x.cpu().numpy(), rows)
