@@ -111,3 +111,42 @@ def test_device_caches_keyed_by_device():
     assert key in basis._dev and basis._dev[key][0] is fwd
     assert basis.plans[0].tables_ready
     assert basis.plans[0].fwd_pairs.device == torch.device("cuda", torch.cuda.current_device())
+
+
+def test_concurrent_host_threads_on_split_path():
+    """Two host threads multiply different batches at the same time through
+    the two-stream split (>= 128 limb-products) and the host pipeline: the
+    fork/join events and copy streams are per host thread, so neither call
+    waits on - or reads - the other's data (capi.cu shared
+    per-device events)."""
+    import threading
+
+    basis = nt.RnsBasis.build(1 << 14, 60, 8, seed=0)
+    batches = [(_batch(basis, 17, 100 * k), _batch(basis, 17, 100 * k + 50)) for k in range(2)]
+    want = [nt.polymul_rns_batch(dev(a), dev(b), basis).cpu().numpy() for a, b in batches]
+    got = [None, None]
+    errors = []
+
+    def work(k):
+        try:
+            torch.cuda.set_device(0)
+            a, b = batches[k]
+            for _ in range(5):
+                da, db = dev(a), dev(b)
+                dev_out = nt.polymul_rns_batch(da, db, basis)
+                host_out = nt.polymul_rns_batch(a, b, basis)
+                torch.cuda.synchronize()
+                if not (np.array_equal(dev_out.cpu().numpy(), want[k]) and
+                        np.array_equal(np.asarray(host_out), want[k])):
+                    errors.append(k)
+            got[k] = dev_out.cpu().numpy()
+        except Exception as exc:  # noqa: BLE001 - reported below
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert all(np.array_equal(g, w) for g, w in zip(got, want))
