@@ -29,6 +29,7 @@ the sweeps' ``tallies`` (uint64[3][4]) are accumulated like the reference.
 
 from __future__ import annotations
 
+import threading
 import weakref
 
 import numpy as np
@@ -55,19 +56,24 @@ RED_BUILTIN, RED_TWO_SUB, RED_ONE_SUB = 0, 1, 2
 
 _PAIRS: dict = {}
 _PAIRS_MAX = 64
+_PAIRS_LOCK = threading.Lock()
 
 
 def _evict(key) -> None:
-    _PAIRS.pop(key, None)
+    with _PAIRS_LOCK:
+        _PAIRS.pop(key, None)
 
 
 def _remember(tw, q: int, entry) -> None:
     key = (id(tw), q, _device.index())
-    if key not in _PAIRS:
-        while len(_PAIRS) >= _PAIRS_MAX:
-            _PAIRS.pop(next(iter(_PAIRS)))
+    with _PAIRS_LOCK:
+        fresh = key not in _PAIRS
+        if fresh:
+            while len(_PAIRS) >= _PAIRS_MAX:
+                _PAIRS.pop(next(iter(_PAIRS)))
+        _PAIRS[key] = entry
+    if fresh:
         weakref.finalize(tw, _evict, key)
-    _PAIRS[key] = entry
 
 
 def register_pairs(tw: torch.Tensor, pairs: torch.Tensor, q: int, w1: int) -> None:
