@@ -56,7 +56,7 @@ RED_BUILTIN, RED_TWO_SUB, RED_ONE_SUB = 0, 1, 2
 
 _PAIRS: dict = {}
 _PAIRS_MAX = 64
-_PAIRS_LOCK = threading.Lock()
+_PAIRS_LOCK = threading.RLock()  # re-entrant: a finalizer may run inside a locked section
 
 
 def _evict(key) -> None:
