@@ -158,7 +158,10 @@ int launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, co
 
 // ---- row kernel dispatch ---------------------------------------------------
 #ifndef NTTB_ROW_PF
-#define NTTB_ROW_PF 1  // L2 prefetch of the rows one resident wave ahead
+// L2 prefetch of the rows one resident wave ahead: measured slower since the
+// launches overlap (PDL): row kernel 0.5213 -> 0.5168 ms without it, cfg2
+// +1.2 % (r2 A/B, 2 runs each); off
+#define NTTB_ROW_PF 0
 #endif
 template <int LOG_R, int FWD, bool MID, int INV, int MODE, int LB>
 int launch_row_t(const RowParams &P, long long rows, cudaStream_t st) {
