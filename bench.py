@@ -8,8 +8,8 @@ A step = one fused polymul of every (ciphertext, limb) pair of a
 [batch, 21, 65536] residue batch (batch ciphertexts per GPU, weak scaling:
 shards are independent ciphertexts, no collective on the data path).  The
 timed region is K steps on the device (CUDA events on the launch stream,
-barrier + synchronize on both sides, max over ranks).  Inputs (2 x 336 MiB at
-the default batch 32) exceed the 126 MB L2, so no flush is needed between steps.
+barrier + synchronize on both sides, max over ranks).  Inputs (2 x 672 MiB at
+the default batch 64) exceed the 126 MB L2, so no flush is needed between steps.
 
 Rank 0 prints ONE JSON line.
 """
@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--batch", type=int, default=32,
+    ap.add_argument("--batch", type=int, default=64,
                     help="ciphertexts per GPU (cfg3: >= 8, SURVEY 8(d); 8 / 16 / 32 / 64 give "
                          "23.1k / 23.5k / 23.8k / 23.9k ct/s on one B200, profiles/r2/NOTES.md)")
     ap.add_argument("--log-n", type=int, default=16)
