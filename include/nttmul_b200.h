@@ -273,6 +273,10 @@ int nttmul_set_split(int log_n, int log_r);
  * stages (more, shorter CTAs) before rows of 1024 words - the latency
  * schedule of a single large transform */
 #define NTTMUL_SCHED_PASSES 3
+/* standalone transforms only: ONE cooperative launch of 2^A CTAs per
+ * polynomial (column stages, grid barrier, row stages) - the latency
+ * schedule of a single transform of 2^13 .. 2^17 words */
+#define NTTMUL_SCHED_GRID 4
 int nttmul_set_schedule(int which, int log_n, int schedule);
 
 /* ---- RNS decomposition / CRT reconstruction (rns.py:82-108) ------------- */

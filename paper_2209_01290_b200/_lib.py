@@ -17,7 +17,7 @@ LIB_NAME = "libnttmul_b200.so"
 LIB_PATH = os.environ.get("NTTMUL_LIB") or os.path.join(HERE, LIB_NAME)
 
 ABI_VERSION = 1
-SCHED_AUTO, SCHED_THREE, SCHED_CLUSTER, SCHED_PASSES = 0, 1, 2, 3
+SCHED_AUTO, SCHED_THREE, SCHED_CLUSTER, SCHED_PASSES, SCHED_GRID = 0, 1, 2, 3, 4
 
 _c_u64 = ctypes.c_uint64
 _c_i64 = ctypes.c_int64

@@ -18,6 +18,7 @@
 #include "nttmul_b200.h"
 #include "ntt_kernels.cuh"
 #include "cluster_kernels.cuh"
+#include "grid_kernels.cuh"
 #include "verify_kernels.cuh"
 #include "crt_kernels.cuh"
 
@@ -261,7 +262,11 @@ inline int pass_plan(int c, int *r) {
   return np;
 }
 
-constexpr int LAT_LOG_R = 10;  // row length of the latency schedule
+// Row length of the latency schedule: 2^10 words, 2^11 at n = 2^17
+// (latency sweep over 2^10 .. 2^13 rows, profiles/r2/latency_rows_r2.jsonl:
+// 2^17 ntt 13.1 -> 11.3 us, intt 12.2 -> 11.6 us; longer rows lose at every
+// smaller size).
+inline int lat_log_r(int log_n) { return log_n >= 17 ? 11 : 10; }
 
 // ---- radix split of n > 4096 into N1 columns x N2 = 2^log_r row length ----
 // Default 2^12 rows; nttmul_set_split picks 2^10 .. 2^13 per size (cfg5
@@ -365,17 +370,14 @@ int launch_cluster(int log_n1, const ClusterParams &P, long long npolys, cudaStr
 
 // Default schedule (NTTMUL_SCHED_AUTO) per size, from the round-2
 // measurements (profiles/r2/NOTES.md).
-// Latency schedule of the standalone transforms: strided passes + rows of
-// 2^10.  Auto (latency_sweep r2, profiles/r2/latency_r2.jsonl): a single
-// forward transform of 2^13, 2^15 or 2^16 words and a single inverse of
-// 2^13 .. 2^17 words (2^16: ntt 9.9 -> 7.9 us, intt 11.7 -> 8.6 us); batches
-// keep the column kernel (one HBM round trip for all column stages).
-inline bool use_passes(int log_n, long long npolys, bool inverse) {
+// Latency schedule of the standalone transforms before the grid kernel:
+// strided passes + rows of 2^10 (2^11 at 2^17), three or four PDL-chained
+// launches (latency_sweep r2, profiles/r2/latency_r2.jsonl: 2^16 ntt 9.9 ->
+// 7.9 us over the column / row kernels).  Superseded by the one-launch grid
+// schedule for single transforms; kept as NTTMUL_SCHED_PASSES.
+inline bool use_passes(int log_n, long long /*npolys*/, bool /*inverse*/) {
   if (log_n <= COL_LOG_R || g_split[log_n]) return false;
-  const int s = g_sched_xform[log_n];
-  if (s == NTTMUL_SCHED_PASSES) return true;
-  if (s != NTTMUL_SCHED_AUTO || npolys != 1) return false;
-  return inverse || log_n == 13 || log_n == 15 || log_n == 16;
+  return g_sched_xform[log_n] == NTTMUL_SCHED_PASSES;
 }
 
 inline bool use_cluster(const int *table, int log_n, long long npolys) {
@@ -391,6 +393,88 @@ inline bool use_cluster(const int *table, int log_n, long long npolys) {
   // half; a cluster CTA waits on its own HBM phases), and the 1024-word
   // split beats the cluster for single transforms.
   return table == g_sched_fused && log_n == COL_LOG_R + 1 && npolys <= 1024;
+}
+
+// ---- grid kernel (one cooperative launch per transform) -------------------
+// Rows of 2^B words, 2^A = n / 2^B CTAs per polynomial, 2^LOG_E elements
+// per thread and pass (grid_kernels.cuh).  Geometry per size from the grid
+// sweep (scripts/grid_sweep.py, profiles/r2/grid_sweep_r2.jsonl): one
+// element pair per thread (LOG_E = 1) up to 2^16, pairs of pairs at 2^17.
+template <int A, int B, int LOG_E, bool INV, int KIND, int LB>
+int launch_grid_t(const GridParams &P, long long npolys, cudaStream_t st) {
+  using G = GridGeom<A, B, LOG_E>;
+  const size_t smem = grid_smem_bytes<A, B, LOG_E>();
+  auto k = grid_kernel<A, B, LOG_E, INV, KIND, LB>;
+  CHECK(smem_optin(k, smem));
+  // every CTA of the launch must be resident at once (grid barrier)
+  static std::atomic<int> cap{0};
+  if (!cap.load()) {
+    int per_sm = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, G::T, smem) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return cuda_status("grid occupancy");
+    cap.store(per_sm * sms);
+  }
+  const long long blocks = npolys << A;
+  if (blocks > cap.load())
+    return fail(NTTMUL_EINVAL, "grid schedule: %lld CTAs exceed the %d co-resident", blocks,
+                cap.load());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(G::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, P);
+  if (e != cudaSuccess) return fail(NTTMUL_ELAUNCH, "grid_kernel: %s", cudaGetErrorString(e));
+  return cuda_status("grid_kernel");
+}
+
+// log_n -> instantiation.  Built with -DNTTB_GRID_SWEEP, the forward
+// (< 2^60 moduli) and inverse kernels of every (A, LOG_E) of the sweep are
+// instantiated too and NTTB_GRID_A / NTTB_GRID_E select one.
+template <bool INV, int KIND, int LB>
+int launch_grid(int log_n, const GridParams &P, long long npolys, cudaStream_t st) {
+#ifdef NTTB_GRID_SWEEP
+  if constexpr ((!INV && LB == 16 && KIND == FWD_FULL) || (INV && LB == 8 && KIND == INV_FULL)) {
+    static const int A = std::getenv("NTTB_GRID_A") ? std::atoi(std::getenv("NTTB_GRID_A")) : 0;
+    static const int E = std::getenv("NTTB_GRID_E") ? std::atoi(std::getenv("NTTB_GRID_E")) : 0;
+#define NTTB_G(LN, AV, EV)                \
+  if (log_n == LN && A == AV && E == EV) \
+    return launch_grid_t<AV, LN - AV, EV, INV, KIND, LB>(P, npolys, st);
+#define NTTB_GE(LN, AV) NTTB_G(LN, AV, 1) NTTB_G(LN, AV, 2) NTTB_G(LN, AV, 3)
+    NTTB_GE(13, 5) NTTB_GE(13, 6)
+    NTTB_GE(14, 6) NTTB_GE(14, 7)
+    NTTB_GE(15, 6) NTTB_GE(15, 7)
+    NTTB_GE(16, 7) NTTB_GE(16, 8)
+    NTTB_GE(17, 7) NTTB_GE(17, 8)
+#undef NTTB_GE
+#undef NTTB_G
+  }
+#endif
+  switch (log_n) {
+    case 13: return launch_grid_t<5, 8, 1, INV, KIND, LB>(P, npolys, st);
+    case 14: return launch_grid_t<7, 7, 1, INV, KIND, LB>(P, npolys, st);
+    case 15: return launch_grid_t<7, 8, 1, INV, KIND, LB>(P, npolys, st);
+    case 16: return launch_grid_t<7, 9, 1, INV, KIND, LB>(P, npolys, st);
+    case 17: return launch_grid_t<7, 10, 2, INV, KIND, LB>(P, npolys, st);
+  }
+  return fail(NTTMUL_EINVAL, "grid schedule: n = 2^%d unsupported", log_n);
+}
+
+// Auto: a single transform (grid sweep r2: 2^16 ntt 7.8-10.5 -> 6.1 us,
+// intt 8.3 -> 6.3 us; 2^13 intt 6.1 -> 5.0 us); batches keep the column /
+// row kernels.
+inline bool use_grid(int log_n, long long npolys) {
+  if (log_n <= COL_LOG_R || log_n > 17 || g_split[log_n]) return false;
+  const int s = g_sched_xform[log_n];
+  if (s == NTTMUL_SCHED_GRID) return true;
+  return s == NTTMUL_SCHED_AUTO && npolys == 1;
 }
 
 constexpr int SMALL_MAX_LOG = 9;  // n <= 2^9 -> small kernel
@@ -414,7 +498,13 @@ int run_forward(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
       return launch_cluster<CL_FWD, 2, LB>(log_n - COL_LOG_R, P, npolys, st);
     }
   }
+  if (use_grid(log_n, npolys)) {
+    GridParams P{a, tw, ls, FIN_PLAIN};
+    return truncate ? launch_grid<false, FWD_TRUNC, LB>(log_n, P, npolys, st)
+                    : launch_grid<false, FWD_FULL, LB>(log_n, P, npolys, st);
+  }
   if (use_passes(log_n, npolys, false)) {
+    const int LAT_LOG_R = lat_log_r(log_n);
     const int c = log_n - LAT_LOG_R;
     int r[4];
     const int np = pass_plan(c, r);
@@ -453,7 +543,13 @@ int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
       return launch_cluster<CL_INV, 2, LB>(log_n - COL_LOG_R, P, npolys, st);
     }
   }
+  if (use_grid(log_n, npolys)) {
+    GridParams P{a, tw, ls, fin};
+    return skip ? launch_grid<true, INV_SKIP, LB>(log_n, P, npolys, st)
+                : launch_grid<true, INV_FULL, LB>(log_n, P, npolys, st);
+  }
   if (use_passes(log_n, npolys, true)) {
+    const int LAT_LOG_R = lat_log_r(log_n);
     const int c = log_n - LAT_LOG_R;
     RowParams R{a, a, nullptr, tw, ls, c, fin, 0};
     CHECK((skip ? launch_row_m<FWD_NONE, false, INV_SKIP, 2, LB>(LAT_LOG_R, R, npolys << c, st)
@@ -656,6 +752,97 @@ int single_limb(Limb *L, u64 q, int mode, u64 mu, int s_in, int s_out,
   return NTTMUL_OK;
 }
 
+// ---- launch-graph cache -----------------------------------------------------
+// A short call (a single transform or product of n >= 2^13: two to four
+// launches) costs ~2.3 us of host time per cudaLaunchKernelEx on the B200
+// hosts (scripts/microbench/launch_cost.cu) - more than its device time.  A
+// call that repeats with identical arguments (pointers, sizes, constants,
+// schedule knobs) is captured into a CUDA graph on its second occurrence
+// and replayed from then on with one cudaGraphLaunch (~2 us for three
+// kernels, programmatic edges kept).  Per host thread; the first occurrence
+// of a key launches directly, so every kernel attribute is already set when
+// the capture runs.  Skipped for work of more than GRAPH_MAX_WORDS words
+// (device-bound), while the caller's stream is itself being captured, and
+// under NTTB_NO_GRAPH=1.
+constexpr long long GRAPH_MAX_WORDS = 1LL << 21;
+std::atomic<unsigned> g_config_epoch{0};  // bumped by set_split / set_schedule
+
+struct GraphEntry {
+  u64 key[16];
+  int nkey = 0;
+  int dev = -1;
+  unsigned epoch = 0;
+  int seen = 0;  // 1 = launched directly once, 2 = graph (or -1: not capturable)
+  cudaGraphExec_t exec = nullptr;
+};
+
+template <class F>
+int run_graphed(const u64 *key, int nkey, long long words, cudaStream_t st, F &&issue) {
+  static const bool off = std::getenv("NTTB_NO_GRAPH") != nullptr;
+  if (off || words > GRAPH_MAX_WORDS) return issue(st);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return issue(st);
+  }
+  if (cs != cudaStreamCaptureStatusNone) return issue(st);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_status("device");
+  constexpr int NE = 16;
+  thread_local GraphEntry table[NE];
+  thread_local int next = 0;
+  thread_local cudaStream_t cap[64] = {};
+  const unsigned epoch = g_config_epoch.load(std::memory_order_relaxed);
+  GraphEntry *hit = nullptr;
+  for (GraphEntry &e : table)
+    if (e.nkey == nkey && e.dev == dev && e.epoch == epoch &&
+        std::memcmp(e.key, key, nkey * sizeof(u64)) == 0) {
+      hit = &e;
+      break;
+    }
+  if (!hit) {  // first occurrence: remember the key, launch directly
+    GraphEntry &e = table[next];
+    next = (next + 1) % NE;
+    if (e.exec) cudaGraphExecDestroy(e.exec);  // (in-flight launches complete)
+    e.exec = nullptr;
+    std::memcpy(e.key, key, nkey * sizeof(u64));
+    e.nkey = nkey;
+    e.dev = dev;
+    e.epoch = epoch;
+    e.seen = 1;
+    return issue(st);
+  }
+  if (hit->seen < 0) return issue(st);
+  if (!hit->exec) {  // second occurrence: capture on a private stream
+    if (dev < 0 || dev >= 64) return issue(st);
+    if (!cap[dev] && cudaStreamCreateWithFlags(&cap[dev], cudaStreamNonBlocking) != cudaSuccess)
+      return cuda_status("graph capture stream");
+    if (cudaStreamBeginCapture(cap[dev], cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      hit->seen = -1;
+      return issue(st);
+    }
+    const int s = issue(cap[dev]);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(cap[dev], &g);
+    cudaGraphExec_t x = nullptr;
+    const bool ok = s == NTTMUL_OK && e == cudaSuccess && g &&
+                    cudaGraphInstantiate(&x, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+      if (std::getenv("NTTB_DEBUG_GRAPH")) std::fprintf(stderr, "graph capture failed: %d %s\n", s, cudaGetErrorString(e));
+      cudaGetLastError();
+      hit->seen = -1;
+      return issue(st);
+    }
+    hit->exec = x;
+    hit->seen = 2;
+    if (std::getenv("NTTB_DEBUG_GRAPH")) std::fprintf(stderr, "graph captured (key %llu)\n", (unsigned long long)key[0]);
+  }
+  if (cudaGraphLaunch(hit->exec, st) != cudaSuccess) return cuda_status("graph launch");
+  return NTTMUL_OK;
+}
+
 TwSet one_table(const u64 *pairs) {
   const ulonglong2 *t = reinterpret_cast<const ulonglong2 *>(pairs);
   return TwSet{t, t, 0};
@@ -778,14 +965,21 @@ int nttmul_ntt_ct(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, int mode,
   ls.num = 1;
   ls.base = 0;
   CHECK(single_limb(&ls.single, q, mode, mu, s_in, s_out, log_n, 1));
-  switch (lazy_bound(q)) {
-    case 16: return run_forward<16>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
-                                    S(stream));
-    case 8: return run_forward<8>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
-                                  S(stream));
-    default: return run_forward<4>(a, one_table(tw_pairs), ls, log_n, batch, truncate != 0,
-                                   S(stream));
-  }
+  const TwSet tw = one_table(tw_pairs);
+  const bool tr = truncate != 0;
+  auto issue = [&](cudaStream_t st) {
+    switch (lazy_bound(q)) {
+      case 16: return run_forward<16>(a, tw, ls, log_n, batch, tr, st);
+      case 8: return run_forward<8>(a, tw, ls, log_n, batch, tr, st);
+      default: return run_forward<4>(a, tw, ls, log_n, batch, tr, st);
+    }
+  };
+  if (log_n <= SMALL_MAX_LOG) return issue(S(stream));  // one launch
+  const u64 key[] = {1, reinterpret_cast<u64>(a), reinterpret_cast<u64>(tw_pairs), q,
+                     static_cast<u64>(mode), mu, static_cast<u64>(s_in),
+                     static_cast<u64>(s_out), static_cast<u64>(tr), static_cast<u64>(log_n),
+                     static_cast<u64>(batch)};
+  return run_graphed(key, sizeof(key) / sizeof(u64), batch << log_n, S(stream), issue);
 }
 
 int nttmul_intt_gs(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, uint64_t half_q,
@@ -804,11 +998,19 @@ int nttmul_intt_gs(uint64_t *a, const uint64_t *tw_pairs, uint64_t q, uint64_t h
   ls.base = 0;
   CHECK(single_limb(&ls.single, q, mode, mu, s_in, s_out, log_n, w1_inv));
   const int fin = scaled ? (skip_first ? FIN_SCALED_SKIP : FIN_SCALED_FULL) : FIN_PLAIN;
+  const TwSet tw = one_table(tw_pairs);
+  const bool skip = skip_first != 0;
   // the inverse uses the same [0, 4q) range for LB 8 and 16
-  return lazy_bound(q) >= 8 ? run_inverse<8>(a, one_table(tw_pairs), ls, log_n, batch,
-                                             skip_first != 0, fin, S(stream))
-                            : run_inverse<4>(a, one_table(tw_pairs), ls, log_n, batch,
-                                             skip_first != 0, fin, S(stream));
+  auto issue = [&](cudaStream_t st) {
+    return lazy_bound(q) >= 8 ? run_inverse<8>(a, tw, ls, log_n, batch, skip, fin, st)
+                              : run_inverse<4>(a, tw, ls, log_n, batch, skip, fin, st);
+  };
+  if (log_n <= SMALL_MAX_LOG) return issue(S(stream));  // one launch
+  const u64 key[] = {2, reinterpret_cast<u64>(a), reinterpret_cast<u64>(tw_pairs), q,
+                     static_cast<u64>(mode), mu, static_cast<u64>(s_in),
+                     static_cast<u64>(s_out), static_cast<u64>(fin), static_cast<u64>(skip),
+                     static_cast<u64>(log_n), static_cast<u64>(batch), w1_inv};
+  return run_graphed(key, sizeof(key) / sizeof(u64), batch << log_n, S(stream), issue);
 }
 
 int nttmul_fused_middle(const uint64_t *ah, const uint64_t *bh, uint64_t *ch,
@@ -930,8 +1132,18 @@ int nttmul_polymul_fused_rns_phases(uint64_t *c, const uint64_t *a, const uint64
   const long long stride = 1LL << log_n;
   TwSet tw{reinterpret_cast<const ulonglong2 *>(fwd_pairs),
            reinterpret_cast<const ulonglong2 *>(inv_pairs), stride};
-  return run_polymul(mode, lbx, c, a, b, workspace, tw, ls, log_n,
-                     batch * num_limbs, phases, S(stream));
+  const long long npolys = batch * num_limbs;
+  auto issue = [&](cudaStream_t st) {
+    return run_polymul(mode, lbx, c, a, b, workspace, tw, ls, log_n, npolys, phases, st);
+  };
+  if (log_n <= COL_LOG_R) return issue(S(stream));  // one launch
+  const u64 key[] = {3, reinterpret_cast<u64>(c), reinterpret_cast<u64>(a),
+                     reinterpret_cast<u64>(b), reinterpret_cast<u64>(limbs),
+                     reinterpret_cast<u64>(fwd_pairs), reinterpret_cast<u64>(inv_pairs),
+                     reinterpret_cast<u64>(workspace), static_cast<u64>(log_n),
+                     static_cast<u64>(num_limbs), static_cast<u64>(batch),
+                     static_cast<u64>(mode), static_cast<u64>(lbx), static_cast<u64>(phases)};
+  return run_graphed(key, sizeof(key) / sizeof(u64), npolys << log_n, S(stream), issue);
 }
 
 int nttmul_set_split(int log_n, int log_r) {
@@ -939,16 +1151,18 @@ int nttmul_set_split(int log_n, int log_r) {
       (log_r != 0 && (log_r < 10 || log_r > 13 || log_n - log_r < 1 || log_n - log_r > 5)))
     return fail(NTTMUL_EINVAL, "set_split(%d, %d)", log_n, log_r);
   g_split[log_n] = log_r;
+  g_config_epoch.fetch_add(1);
   return NTTMUL_OK;
 }
 
 int nttmul_set_schedule(int which, int log_n, int schedule) {
   if (which < 0 || which > 1 || log_n < COL_LOG_R + 1 || log_n > NTTMUL_MAX_LOG_N ||
-      schedule < NTTMUL_SCHED_AUTO || schedule > NTTMUL_SCHED_PASSES ||
-      (schedule == NTTMUL_SCHED_PASSES && which == 0) ||
+      schedule < NTTMUL_SCHED_AUTO || schedule > NTTMUL_SCHED_GRID ||
+      (schedule >= NTTMUL_SCHED_PASSES && which == 0) ||
       (schedule == NTTMUL_SCHED_CLUSTER && log_n > COL_LOG_R + 4))
     return fail(NTTMUL_EINVAL, "set_schedule(%d, %d, %d)", which, log_n, schedule);
   (which == 0 ? g_sched_fused : g_sched_xform)[log_n] = schedule;
+  g_config_epoch.fetch_add(1);
   return NTTMUL_OK;
 }
 

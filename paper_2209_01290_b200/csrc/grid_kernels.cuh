@@ -1,0 +1,220 @@
+// grid_kernels.cuh - one-launch latency schedule of a standalone transform.
+//
+// A single forward / inverse transform of n = 2^13 .. 2^17 words is a few
+// microseconds of chained launches: the latency schedule of capi.cu
+// (strided column passes + 1024-word rows) takes three launches for 2^16,
+// each paying a kernel boundary and an L2 round trip.  Here the transform
+// is ONE cooperative launch of 2^A CTAs per polynomial, n = 2^A rows x 2^B
+// words:
+//   column phase  CTA c owns columns [c W, c W + W), W = 2^(B-A): all 2^A
+//                 rows of them (W-word coalesced segments), and runs the A
+//                 column stages (half-size k >= 2^B) in register passes
+//                 through shared memory;
+//   grid barrier  (cooperative_groups::grid_group::sync);
+//   row phase     CTA c owns row c and runs the B row stages.
+// The inverse runs the phases mirrored.  A single transform is a latency
+// chain per warp (ncu r2: ~5.6 stall cycles per issued instruction, one or
+// two warps per SM), so threads own only 2^LOG_E elements per pass: 2^16
+// words run as 512 short warps of 4 elements instead of 256 long ones of 8.
+// Butterflies, twiddles, lazy ranges and the final canonicalisation are the
+// radix.cuh units of every other schedule, so outputs are bit-identical to
+// them and to the reference's merged transforms (_kernels.pyx:52-129).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "ntt_kernels.cuh"
+
+namespace nttb {
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
+}
+
+struct GridParams {
+  u64 *a;
+  TwSet tw;
+  LimbSet limbs;
+  int fin;  // inverse: FinalMode of the global last stage
+};
+
+// 2^B-word rows, 2^A per polynomial, 2^LOG_E elements per thread and pass
+// (passes of <= LOG_E stages).
+template <int A, int B, int LOG_E>
+struct GridGeom {
+  static constexpr int T = 1 << (B - LOG_E);  // threads per CTA
+  static constexpr int W = 1 << (B - A);      // columns per CTA in the column phase
+  static constexpr int PADN = (1 << B) + (1 << B) / 16;
+  __device__ __forceinline__ static int idx(int o) { return o + (o >> 4); }
+  // K stages as passes of <= LOG_E stages (balanced)
+  template <int K>
+  struct Plan {
+    static constexpr int NPASS = (K + LOG_E - 1) / LOG_E;
+    __host__ __device__ static constexpr int R(int i) {
+      return K / NPASS + (i < K % NPASS ? 1 : 0);
+    }
+    __host__ __device__ static constexpr int S0(int i) { return i == 0 ? 0 : S0(i - 1) + R(i - 1); }
+  };
+};
+
+// Shared-memory bytes of a grid kernel: the row (padded) + its twiddles.
+template <int A, int B, int LOG_E>
+constexpr size_t grid_smem_bytes() {
+  return GridGeom<A, B, LOG_E>::PADN * sizeof(u64) + (size_t(1) << B) * sizeof(ulonglong2);
+}
+
+// One pass of R stages starting at stage S0 of a 2^B-element transform
+// spread over the CTA: units of 2^R elements spaced 2^LK apart (the
+// radix.cuh unit), UNITS / T per thread.  Element o lives at GridGeom::idx(o)
+// in shared memory or, for FROM_G / TO_G, at gaddr(o) in global memory.
+// Forward passes stop after TS stages (truncated transforms); inverse
+// passes run stages TS-1 .. 0, the last with inv_stage0 when STAGE0 (global
+// stage 0, FinalMode fin).  CANON: canonicalise the forward output.
+template <int LB, int A, int B, int LOG_E, int S0, int R, bool INV, bool FROM_G, bool TO_G, int TS,
+          bool STAGE0, bool CANON, class GA>
+__device__ __forceinline__ void grid_pass(u64 *__restrict__ sm, u64 *__restrict__ g, GA gaddr,
+                                          const ulonglong2 *__restrict__ tw, const Limb &L,
+                                          const Mod &M, int fin) {
+  using G = GridGeom<A, B, LOG_E>;
+  constexpr int LK = B - S0 - R;
+  constexpr int UNITS = 1 << (B - R);
+  static_assert(UNITS % G::T == 0, "grid pass: every thread owns the same number of units");
+#pragma unroll
+  for (int w = 0; w < UNITS / G::T; ++w) {
+    const int u = threadIdx.x + w * G::T;
+    const int grp = u >> LK;
+    const int o0 = (grp << (B - S0)) + (u & ((1 << LK) - 1));
+    u64 x[1][1 << R];
+#pragma unroll
+    for (int e = 0; e < (1 << R); ++e) {
+      const int o = o0 + (e << LK);
+      x[0][e] = FROM_G ? g[gaddr(o)] : sm[G::idx(o)];
+    }
+    const u64 B0 = (1ULL << S0) + static_cast<u64>(grp);
+    if constexpr (!INV) {
+      fwd_radix<LB, R, TS, 1>(x, B0, tw, M);  // starts with a reducing stage
+      if constexpr (CANON) {
+#pragma unroll
+        for (int e = 0; e < (1 << R); ++e) x[0][e] = canon_fwd<LB>(x[0][e], M);
+      }
+    } else if constexpr (STAGE0) {
+      inv_radix<LB, R, TS, 1, 1>(x, B0, tw, M);
+      inv_stage0<LB, R, 1>(x, B0, tw, L, M, fin);
+    } else {
+      inv_radix<LB, R, TS, 0, 1>(x, B0, tw, M);
+    }
+#pragma unroll
+    for (int e = 0; e < (1 << R); ++e) {
+      const int o = o0 + (e << LK);
+      if (TO_G)
+        g[gaddr(o)] = x[0][e];
+      else
+        sm[G::idx(o)] = x[0][e];
+    }
+  }
+}
+
+// Column phase: the A column stages of this CTA's W columns.  Element
+// o = row * W + col stands for word (row << B) + c0 + col of the
+// polynomial; in that numbering the column stages are exactly stages
+// 0 .. A-1 of a 2^B-element transform (group of stage s = row >> (A - s),
+// twiddle tw[2^s + group] of the global table), and consecutive units
+// step over the columns first, so warps touch contiguous W-word segments.
+template <int LB, int A, int B, int LOG_E, bool INV, int I>
+__device__ __forceinline__ void grid_cols(u64 *sm, u64 *g, int c0, const ulonglong2 *tw,
+                                          const Limb &L, const Mod &M, int fin) {
+  using P = typename GridGeom<A, B, LOG_E>::template Plan<A>;
+  constexpr int NP = P::NPASS;
+  if constexpr (I >= 0 && I < NP) {
+    constexpr int S0 = P::S0(I), R = P::R(I);
+    auto gaddr = [c0](int o) {
+      return (static_cast<long long>(o >> (B - A)) << B) + c0 + (o & ((1 << (B - A)) - 1));
+    };
+    if constexpr (!INV) {
+      grid_pass<LB, A, B, LOG_E, S0, R, false, I == 0, I == NP - 1, R, false, false>(
+          sm, g, gaddr, tw, L, M, fin);
+      if constexpr (I + 1 < NP) __syncthreads();
+      grid_cols<LB, A, B, LOG_E, false, I + 1>(sm, g, c0, tw, L, M, fin);
+    } else {
+      grid_pass<LB, A, B, LOG_E, S0, R, true, I == NP - 1, I == 0, R, I == 0, false>(
+          sm, g, gaddr, tw, L, M, fin);
+      if constexpr (I > 0) __syncthreads();
+      grid_cols<LB, A, B, LOG_E, true, I - 1>(sm, g, c0, tw, L, M, fin);
+    }
+  }
+}
+
+// Row phase: the B row stages of one row (twiddles staged at stw, base 1:
+// row-local stage s, group g -> stw[2^s + g]).  Forward passes run upward
+// from row-local stage 0 (the first reads global, the last canonicalises
+// and writes global); inverse passes run downward (the first reads global,
+// the last writes global, lazy).
+template <int LB, int A, int B, int LOG_E, bool INV, int KIND, int I>
+__device__ __forceinline__ void grid_row(u64 *sm, u64 *row, const ulonglong2 *stw, const Limb &L,
+                                         const Mod &M) {
+  using P = typename GridGeom<A, B, LOG_E>::template Plan<B>;
+  constexpr int NP = P::NPASS;
+  if constexpr (I >= 0 && I < NP) {
+    constexpr int S0 = P::S0(I), R = P::R(I);
+    constexpr bool TOP = S0 + R == B;  // the pass holding row-local stage B-1
+    auto gaddr = [](int o) { return static_cast<long long>(o); };
+    if constexpr (!INV) {
+      constexpr int TS = (TOP && KIND == FWD_TRUNC) ? R - 1 : R;
+      grid_pass<LB, A, B, LOG_E, S0, R, false, I == 0, I == NP - 1, TS, false, I == NP - 1>(
+          sm, row, gaddr, stw, L, M, FIN_LAZY);
+      if constexpr (I + 1 < NP) __syncthreads();
+      grid_row<LB, A, B, LOG_E, false, KIND, I + 1>(sm, row, stw, L, M);
+    } else {
+      constexpr int TS = (TOP && KIND == INV_SKIP) ? R - 1 : R;
+      grid_pass<LB, A, B, LOG_E, S0, R, true, I == NP - 1, I == 0, TS, false, false>(
+          sm, row, gaddr, stw, L, M, FIN_LAZY);
+      if constexpr (I > 0) __syncthreads();
+      grid_row<LB, A, B, LOG_E, true, KIND, I - 1>(sm, row, stw, L, M);
+    }
+  }
+}
+
+// KIND: FwdKind (INV false) or InvKind (INV true)
+template <int A, int B, int LOG_E, bool INV, int KIND, int LB>
+__global__ void __launch_bounds__(GridGeom<A, B, LOG_E>::T) grid_kernel(const GridParams P) {
+  using G = GridGeom<A, B, LOG_E>;
+  static_assert(A >= 1 && B >= A, "grid geometry: at least one column per CTA");
+  extern __shared__ u64 sm[];
+  const long long poly = blockIdx.x >> A;
+  const int r = static_cast<int>(blockIdx.x & ((1u << A) - 1));
+  int limb;
+  const Limb &L = *limb_ptr(P.limbs, poly, limb);
+  const Mod M = mod_for<LB>(L.q);
+  const ulonglong2 *tw = (INV ? P.tw.inv : P.tw.fwd) + limb * P.tw.stride;
+  u64 *a = P.a + (poly << (A + B));
+  const u64 rowbase = (1ULL << A) + r;
+  u64 *row = a + (static_cast<long long>(r) << B);
+  // The row's twiddles - tw[(rowbase << s) + g] at row-local stage s - are
+  // staged into shared memory at stw[(1 << s) + g] first (async; in the
+  // forward transform this overlaps the column phase), so the row passes
+  // wait on shared memory instead of an L2 round trip per pass.
+  ulonglong2 *stw = reinterpret_cast<ulonglong2 *>(sm + G::PADN);
+  for (int i = threadIdx.x; i < (1 << B); i += G::T) {
+    if (i == 0) continue;
+    const int s = 31 - __clz(i);
+    cp_async16(stw + i, tw + ((rowbase << s) + (i - (1 << s))));
+  }
+  cp_async_commit();
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  constexpr int NPC = G::template Plan<A>::NPASS;
+  constexpr int NPR = G::template Plan<B>::NPASS;
+  if constexpr (!INV) {
+    grid_cols<LB, A, B, LOG_E, false, 0>(sm, a, r * G::W, tw, L, M, FIN_LAZY);
+    cp_async_wait<0>();
+    grid.sync();  // (includes the CTA barrier that publishes stw)
+    grid_row<LB, A, B, LOG_E, false, KIND, 0>(sm, row, stw, L, M);
+  } else {
+    cp_async_wait<0>();
+    __syncthreads();
+    grid_row<LB, A, B, LOG_E, true, KIND, NPR - 1>(sm, row, stw, L, M);
+    grid.sync();
+    grid_cols<LB, A, B, LOG_E, true, NPC - 1>(sm, a, r * G::W, tw, L, M, P.fin);
+  }
+}
+
+}  // namespace nttb

@@ -106,7 +106,8 @@ def test_cluster_standalone_transforms(log_n):
 
 
 def test_schedule_knob_rejects_bad_arguments():
-    for args in ((2, 14, 1), (0, 12, 1), (0, 17, 2), (0, 14, 3), (1, 18, 1), (1, 17, 2)):
+    for args in ((2, 14, 1), (0, 12, 1), (0, 17, 2), (0, 14, 3), (0, 14, 4), (1, 14, 5),
+                 (1, 18, 1), (1, 17, 2)):
         with pytest.raises(nt._lib.NttmulError):
             lib.call("nttmul_set_schedule", *args)
 
@@ -206,3 +207,68 @@ def test_batched_transforms_large_batches(log_n, batch):
     nt.kernels.intt_gs(x, plan.tw_inv, plan.q, (plan.q + 1) // 2, *plan.red_args[1:], True,
                        False, None)
     assert np.array_equal(x.cpu().numpy(), rows)
+
+
+# ---- one-launch grid schedule (NTTMUL_SCHED_GRID, csrc/grid_kernels.cuh) ---
+
+@pytest.mark.parametrize("bits", [59, 61, 62])  # lazy bounds 16, 8, 4
+@pytest.mark.parametrize("log_n", [13, 14, 15, 16, 17])
+@pytest.mark.parametrize("batch", [1, 3])
+def test_grid_schedule_bit_exact(log_n, batch, bits):
+    """The cooperative one-launch transform for ntt_ct (full / truncated)
+    and intt_gs (scaled full / skip_first / plain), every lazy-bound class
+    of moduli, single and batched (ragged) launches."""
+    n = 1 << log_n
+    plan = nt.build_plan(n, bits=bits, seed=3)
+    f, v = oracle.twiddles(plan.q, plan.psi, log_n)
+    rows = np.stack([rand(plan.q, n, 61 + i) for i in range(batch)])
+    args = plan.red_args
+    half_q = (plan.q + 1) // 2
+    with schedule(1, log_n, lib.SCHED_GRID):
+        for truncate in (False, True):
+            want = rows.copy()
+            for w in want:
+                oracle.ntt_ct(w, f, *args, truncate)
+            x = dev(rows)
+            nt.kernels.ntt_ct(x, plan.tw_fwd, *args, truncate, None)
+            assert np.array_equal(x.cpu().numpy(), want), f"ntt_ct truncate={truncate}"
+        for scaled, skip in ((True, False), (True, True), (False, False)):
+            want = rows.copy()
+            for w in want:
+                oracle.intt_gs(w, v, plan.q, half_q, *args[1:], scaled, skip)
+            x = dev(rows)
+            nt.kernels.intt_gs(x, plan.tw_inv, plan.q, half_q, *args[1:], scaled, skip, None)
+            assert np.array_equal(x.cpu().numpy(), want), f"intt scaled={scaled} skip={skip}"
+
+
+def test_grid_schedule_edge_values():
+    """All-(q-1) input and a lone x^(n-1) through the grid transforms: the
+    forward / inverse round trip returns them and the forward matches the
+    oracle (largest lazy intermediates)."""
+    n = 1 << 16
+    plan = nt.build_plan(n, bits=59, seed=9)
+    f, _ = oracle.twiddles(plan.q, plan.psi, 16)
+    top = np.full((1, n), plan.q - 1, dtype=np.uint64)
+    mono = np.zeros((1, n), dtype=np.uint64)
+    mono[0, n - 1] = 1
+    with schedule(1, 16, lib.SCHED_GRID):
+        for rows in (top, mono):
+            want = rows.copy()
+            oracle.ntt_ct(want[0], f, *plan.red_args, False)
+            x = dev(rows)
+            nt.kernels.ntt_ct(x, plan.tw_fwd, *plan.red_args, False, None)
+            assert np.array_equal(x.cpu().numpy(), want)
+            nt.kernels.intt_gs(x, plan.tw_inv, plan.q, (plan.q + 1) // 2, *plan.red_args[1:],
+                               True, False, None)
+            assert np.array_equal(x.cpu().numpy(), rows)
+
+
+def test_grid_schedule_rejects_oversized_batch():
+    """A forced grid launch larger than the co-resident CTA count fails
+    loudly (no silent deadlock, no fallback)."""
+    n = 1 << 17
+    plan = nt.build_plan(n, bits=59, seed=1)
+    x = torch.zeros((64, n), dtype=torch.uint64, device="cuda")
+    with schedule(1, 17, lib.SCHED_GRID):
+        with pytest.raises(nt._lib.NttmulError):
+            nt.kernels.ntt_ct(x, plan.tw_fwd, *plan.red_args, False, None)
