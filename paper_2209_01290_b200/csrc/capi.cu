@@ -400,8 +400,29 @@ inline bool use_cluster(const int *table, int log_n, long long npolys) {
 // per thread and pass (grid_kernels.cuh).  Geometry per size from the grid
 // sweep (scripts/grid_sweep.py, profiles/r2/grid_sweep_r2.jsonl): one
 // element pair per thread (LOG_E = 1) up to 2^16, pairs of pairs at 2^17.
+// The grid barrier slot of the next launch (round-robin over GRID_SLOTS;
+// nullptr = cooperative launch + cooperative_groups grid sync, selected by
+// NTTB_GRID_COOP=1).
+int grid_barrier_slot(unsigned **slot) {
+  static const bool coop = std::getenv("NTTB_GRID_COOP") != nullptr;
+  *slot = nullptr;
+  if (coop) return NTTMUL_OK;
+  static std::atomic<unsigned> ticket{0};
+  thread_local unsigned *base[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cuda_status("device");
+  if (!base[dev]) {
+    void *p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_grid_barriers) != cudaSuccess)
+      return cuda_status("grid barrier slots");
+    base[dev] = static_cast<unsigned *>(p);
+  }
+  *slot = base[dev] + ticket.fetch_add(1, std::memory_order_relaxed) % GRID_SLOTS;
+  return NTTMUL_OK;
+}
+
 template <int A, int B, int LOG_E, bool INV, int KIND, int LB>
-int launch_grid_t(const GridParams &P, long long npolys, cudaStream_t st) {
+int launch_grid_t(GridParams P, long long npolys, cudaStream_t st) {
   using G = GridGeom<A, B, LOG_E>;
   const size_t smem = grid_smem_bytes<A, B, LOG_E>();
   auto k = grid_kernel<A, B, LOG_E, INV, KIND, LB>;
@@ -420,6 +441,7 @@ int launch_grid_t(const GridParams &P, long long npolys, cudaStream_t st) {
   if (blocks > cap.load())
     return fail(NTTMUL_EINVAL, "grid schedule: %lld CTAs exceed the %d co-resident", blocks,
                 cap.load());
+  CHECK(grid_barrier_slot(&P.barrier));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(blocks));
   cfg.blockDim = dim3(G::T);
@@ -429,7 +451,7 @@ int launch_grid_t(const GridParams &P, long long npolys, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = P.barrier ? 0 : 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k, P);
   if (e != cudaSuccess) return fail(NTTMUL_ELAUNCH, "grid_kernel: %s", cudaGetErrorString(e));
   return cuda_status("grid_kernel");
@@ -467,14 +489,16 @@ int launch_grid(int log_n, const GridParams &P, long long npolys, cudaStream_t s
   return fail(NTTMUL_EINVAL, "grid schedule: n = 2^%d unsupported", log_n);
 }
 
-// Auto: a single transform (grid sweep r2: 2^16 ntt 7.8-10.5 -> 6.1 us,
-// intt 8.3 -> 6.3 us; 2^13 intt 6.1 -> 5.0 us); batches keep the column /
-// row kernels.
+// Auto: up to 4 polynomials per call (grid sweep r2, grid_default_r2 /
+// grid_batch_r2.jsonl: one 2^16 ntt 8.1-9.3 -> 6.3 us, intt 8.6 -> 6.4 us;
+// two 2^16 11.0 -> 6.8 us, four 11.6 -> 9.0 us; 2^14 x 4 even, x 8 slower);
+// larger batches keep the column / row kernels.  Every geometry holds
+// 4 x 2^A CTAs co-resident.
 inline bool use_grid(int log_n, long long npolys) {
   if (log_n <= COL_LOG_R || log_n > 17 || g_split[log_n]) return false;
   const int s = g_sched_xform[log_n];
   if (s == NTTMUL_SCHED_GRID) return true;
-  return s == NTTMUL_SCHED_AUTO && npolys == 1;
+  return s == NTTMUL_SCHED_AUTO && npolys <= 4;
 }
 
 constexpr int SMALL_MAX_LOG = 9;  // n <= 2^9 -> small kernel
@@ -499,7 +523,7 @@ int run_forward(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
     }
   }
   if (use_grid(log_n, npolys)) {
-    GridParams P{a, tw, ls, FIN_PLAIN};
+    GridParams P{a, tw, ls, FIN_PLAIN, nullptr};
     return truncate ? launch_grid<false, FWD_TRUNC, LB>(log_n, P, npolys, st)
                     : launch_grid<false, FWD_FULL, LB>(log_n, P, npolys, st);
   }
@@ -544,7 +568,7 @@ int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
     }
   }
   if (use_grid(log_n, npolys)) {
-    GridParams P{a, tw, ls, fin};
+    GridParams P{a, tw, ls, fin, nullptr};
     return skip ? launch_grid<true, INV_SKIP, LB>(log_n, P, npolys, st)
                 : launch_grid<true, INV_FULL, LB>(log_n, P, npolys, st);
   }

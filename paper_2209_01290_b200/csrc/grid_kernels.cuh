@@ -4,13 +4,13 @@
 // microseconds of chained launches: the latency schedule of capi.cu
 // (strided column passes + 1024-word rows) takes three launches for 2^16,
 // each paying a kernel boundary and an L2 round trip.  Here the transform
-// is ONE cooperative launch of 2^A CTAs per polynomial, n = 2^A rows x 2^B
+// is ONE launch of 2^A co-resident CTAs per polynomial, n = 2^A rows x 2^B
 // words:
 //   column phase  CTA c owns columns [c W, c W + W), W = 2^(B-A): all 2^A
 //                 rows of them (W-word coalesced segments), and runs the A
 //                 column stages (half-size k >= 2^B) in register passes
 //                 through shared memory;
-//   grid barrier  (cooperative_groups::grid_group::sync);
+//   grid barrier  (slot_barrier below, or cooperative_groups' grid sync);
 //   row phase     CTA c owns row c and runs the B row stages.
 // The inverse runs the phases mirrored.  A single transform is a latency
 // chain per warp (ncu r2: ~5.6 stall cycles per issued instruction, one or
@@ -35,8 +35,38 @@ struct GridParams {
   u64 *a;
   TwSet tw;
   LimbSet limbs;
-  int fin;  // inverse: FinalMode of the global last stage
+  int fin;             // inverse: FinalMode of the global last stage
+  unsigned *barrier;   // the launch's grid barrier word (nullptr: cooperative launch)
 };
+
+// Grid barrier of a plain (non-cooperative) launch whose CTAs are all
+// co-resident (the host checks the grid against the occupancy): one
+// counter word per launch, in a slot the host hands out round-robin.  The
+// arrivals add up to exactly 2^31 (CTA 0 adds 2^31 - (n - 1), the others
+// 1), so the barrier is complete when bit 31 flips, and the word is left in
+// a valid state for its next user (a replay of the same graph, or the
+// launch that draws the slot GRID_SLOTS launches later) without a reset -
+// the flip-bit scheme of cooperative_groups' grid sync, minus the
+// cooperative launch, which costs ~2 us more per call when replayed from a
+// graph (scripts/microbench/launch_floor.cu).
+constexpr int GRID_SLOTS = 4096;
+__device__ unsigned g_grid_barriers[GRID_SLOTS];
+
+__device__ __forceinline__ void slot_barrier(unsigned *bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+    // release / acquire at gpu scope: cumulative over the CTA's writes,
+    // which the CTA barriers order before / after thread 0's operations
+    unsigned old, v;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;"
+                 : "=r"(old) : "l"(bar), "r"(nb) : "memory");
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (((old ^ v) & 0x80000000u) == 0);
+  }
+  __syncthreads();
+}
 
 // 2^B-word rows, 2^A per polynomial, 2^LOG_E elements per thread and pass
 // (passes of <= LOG_E stages).
@@ -200,19 +230,24 @@ __global__ void __launch_bounds__(GridGeom<A, B, LOG_E>::T) grid_kernel(const Gr
     cp_async16(stw + i, tw + ((rowbase << s) + (i - (1 << s))));
   }
   cp_async_commit();
-  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  auto grid_sync = [&] {
+    if (P.barrier)
+      slot_barrier(P.barrier);
+    else
+      cooperative_groups::this_grid().sync();
+  };
   constexpr int NPC = G::template Plan<A>::NPASS;
   constexpr int NPR = G::template Plan<B>::NPASS;
   if constexpr (!INV) {
     grid_cols<LB, A, B, LOG_E, false, 0>(sm, a, r * G::W, tw, L, M, FIN_LAZY);
     cp_async_wait<0>();
-    grid.sync();  // (includes the CTA barrier that publishes stw)
+    grid_sync();  // (includes the CTA barrier that publishes stw)
     grid_row<LB, A, B, LOG_E, false, KIND, 0>(sm, row, stw, L, M);
   } else {
     cp_async_wait<0>();
     __syncthreads();
     grid_row<LB, A, B, LOG_E, true, KIND, NPR - 1>(sm, row, stw, L, M);
-    grid.sync();
+    grid_sync();
     grid_cols<LB, A, B, LOG_E, true, NPC - 1>(sm, a, r * G::W, tw, L, M, P.fin);
   }
 }

@@ -12,3 +12,5 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r
 timeout 600 python bench.py --log-n 14 --limbs 8 --batch 64 --no-cpu-baseline > gpurun_out/re_bench_cfg2.json 2>&1
 timeout 600 python bench.py --log-n 17 --limbs 32 --batch 8 --no-cpu-baseline > gpurun_out/re_bench_cfg4.json 2>&1
 NTTB_BENCH_SHARE_GPU=1 timeout 600 python bench.py --gpus 2 --no-cpu-baseline > gpurun_out/re_bench_share2.json 2>&1
+timeout 600 python scripts/grid_sweep.py > gpurun_out/re_grid.jsonl 2>&1
+timeout 300 python scripts/host_overhead.py > gpurun_out/re_host_overhead.jsonl 2>&1

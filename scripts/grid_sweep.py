@@ -73,8 +73,13 @@ VALID = {13: (5, 6), 14: (6, 7), 15: (6, 7), 16: (7, 8), 17: (7, 8)}
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, nargs="+", default=[1],
+                    help="polynomials per call (the grid launch holds batch x 2^A CTAs)")
+    args = ap.parse_args()
     a_env = int(os.environ.get("NTTB_GRID_A", "0"))
-    for log_n in range(13, 18):
+    for log_n, batch in [(ln, b) for b in args.batch for ln in range(13, 18)]:
         if a_env and a_env not in VALID[log_n]:  # (sweep library only)
             continue
         n = 1 << log_n
@@ -83,20 +88,22 @@ def main():
         pf, _ = nt.kernels._pairs_for(plan.tw_fwd, q)
         pi, w1 = nt.kernels._pairs_for(plan.tw_inv, q)
         src = torch.from_numpy(np.random.default_rng(log_n).integers(
-            0, q, (1, n), dtype=np.uint64)).cuda()
+            0, q, (batch, n), dtype=np.uint64)).cuda()
         x = torch.empty_like(src)
-        rec = {"log_n": log_n, "grid_a": a_env, "grid_e": int(os.environ.get("NTTB_GRID_E", "2"))}
+        rec = {"log_n": log_n, "batch": batch, "grid_a": a_env,
+               "grid_e": int(os.environ.get("NTTB_GRID_E", "0"))}
         outs, fns = {}, {}
-        for sched, name in ((lib.SCHED_PASSES, "default"), (lib.SCHED_GRID, "grid")):
+        base = lib.SCHED_PASSES if batch == 1 else lib.SCHED_AUTO  # (auto: column / row)
+        for sched, name in ((base, "default"), (lib.SCHED_GRID, "grid")):
             lib.call("nttmul_set_schedule", 1, log_n, sched)
 
             def fwd():
                 lib.call("nttmul_ntt_ct", x.data_ptr(), pf.data_ptr(), q, mode, mu, s_in, s_out, 0,
-                         log_n, 1, torch.cuda.current_stream().cuda_stream)
+                         log_n, batch, torch.cuda.current_stream().cuda_stream)
 
             def inv():
                 lib.call("nttmul_intt_gs", x.data_ptr(), pi.data_ptr(), q, (q + 1) // 2, mode, mu,
-                         s_in, s_out, 1, 0, log_n, 1, w1, torch.cuda.current_stream().cuda_stream)
+                         s_in, s_out, 1, 0, log_n, batch, w1, torch.cuda.current_stream().cuda_stream)
 
             x.copy_(src)
             base = x.clone()

@@ -62,6 +62,35 @@ static double graph_us(F issue, cudaStream_t st) {
   return ms * 1e3 / 200;
 }
 
+// per call, `calls` separate submissions (no graph batching): the device
+// timeline when the host submits one call at a time
+template <class F>
+static double stream_us(F issue, cudaStream_t st, int calls = 50) {
+  for (int i = 0; i < 5; ++i) issue();
+  cudaStreamSynchronize(st);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < calls; ++i) issue();
+  cudaEventRecord(e1, st);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  return ms * 1e3 / calls;
+}
+
+template <class F>
+static cudaGraphExec_t one_graph(F issue, cudaStream_t st) {
+  cudaGraph_t g;
+  cudaGraphExec_t x;
+  cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  issue();
+  cudaStreamEndCapture(st, &g);
+  cudaGraphInstantiate(&x, g, 0);
+  return x;
+}
+
 int main() {
   cudaStream_t st;
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
@@ -115,6 +144,26 @@ int main() {
     std::printf("{\"blocks\": %d, \"plain_us\": %.2f, \"coop_gridsync_us\": %.2f, \"pdl_x3_us\": %.2f, "
                 "\"coop_nosync_us\": %.2f, \"custom_barrier_us\": %.2f, \"custom_barrier_coop_us\": %.2f}\n",
                 blocks, plain, grid, pdl3, coop0, cust, cust_coop);
+  }
+  {
+    auto coop1 = [&] {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(128);
+      cfg.blockDim = dim3(256);
+      cfg.stream = st;
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeCooperative;
+      a[0].val.cooperative = 1;
+      cfg.attrs = a;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, k_grid, p);
+    };
+    auto plain1 = [&] { k_plain<<<128, 256, 0, st>>>(p); };
+    cudaGraphExec_t gc = one_graph(coop1, st), gp = one_graph(plain1, st);
+    std::printf("{\"separate_calls\": 50, \"plain_direct_us\": %.2f, \"plain_graph_us\": %.2f, "
+                "\"coop_sync_direct_us\": %.2f, \"coop_sync_graph_us\": %.2f}\n",
+                stream_us(plain1, st), stream_us([&] { cudaGraphLaunch(gp, st); }, st),
+                stream_us(coop1, st), stream_us([&] { cudaGraphLaunch(gc, st); }, st));
   }
   std::printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
