@@ -273,10 +273,11 @@ int nttmul_set_split(int log_n, int log_r);
  * stages (more, shorter CTAs) before rows of 1024 words - the latency
  * schedule of a single large transform */
 #define NTTMUL_SCHED_PASSES 3
-/* standalone transforms only: ONE launch of 2^A co-resident CTAs per
- * polynomial (column stages, grid barrier, row stages) - the latency
- * schedule of up to a few transforms of 2^13 .. 2^17 words (default for
- * <= 4 polynomials per call); a forced launch larger than the co-resident
+/* ONE launch of 2^A co-resident CTAs per polynomial (column stages, grid
+ * barrier, row stages; the fused product: forward columns, barrier, rows
+ * with the Karatsuba middle, barrier, inverse columns) - the latency
+ * schedule of up to a few transforms / limb-products of 2^13 .. 2^17 words
+ * (default for <= 4 per call); a forced launch larger than the co-resident
  * CTA count fails with NTTMUL_EINVAL */
 #define NTTMUL_SCHED_GRID 4
 int nttmul_set_schedule(int which, int log_n, int schedule);

@@ -489,6 +489,70 @@ int launch_grid(int log_n, const GridParams &P, long long npolys, cudaStream_t s
   return fail(NTTMUL_EINVAL, "grid schedule: n = 2^%d unsupported", log_n);
 }
 
+// Fused product in one launch (grid_fused_kernel): rows as for the
+// standalone grid schedule, one element pair per thread.  Returns
+// NTTB_DECLINED when the launch would not fit co-resident and the schedule
+// was not forced.
+constexpr int NTTB_DECLINED = -1;
+
+template <int A, int B, int MODE, int LB>
+int launch_grid_fused_t(GridFusedParams P, long long npolys, bool forced, cudaStream_t st) {
+  using G = GridGeom<A, B, 1>;
+  const size_t smem = grid_fused_smem_bytes<A, B>();
+  auto k = grid_fused_kernel<A, B, MODE, LB>;
+  CHECK(smem_optin(k, smem));
+  static std::atomic<int> cap{0};
+  if (!cap.load()) {
+    int per_sm = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, G::T, smem) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return cuda_status("grid occupancy");
+    cap.store(per_sm * sms);
+  }
+  const long long blocks = npolys << A;
+  if (blocks > cap.load()) {
+    if (!forced) return NTTB_DECLINED;
+    return fail(NTTMUL_EINVAL, "grid schedule: %lld CTAs exceed the %d co-resident", blocks,
+                cap.load());
+  }
+  CHECK(grid_barrier_slot(&P.barrier));
+  if (!P.barrier) return fail(NTTMUL_EINVAL, "fused grid schedule needs a barrier slot");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(G::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, P);
+  if (e != cudaSuccess)
+    return fail(NTTMUL_ELAUNCH, "grid_fused_kernel: %s", cudaGetErrorString(e));
+  return cuda_status("grid_fused_kernel");
+}
+
+template <int MODE, int LB>
+int launch_grid_fused(int log_n, const GridFusedParams &P, long long npolys, bool forced,
+                      cudaStream_t st) {
+  switch (log_n) {
+    case 13: return launch_grid_fused_t<5, 8, MODE, LB>(P, npolys, forced, st);
+    case 14: return launch_grid_fused_t<7, 7, MODE, LB>(P, npolys, forced, st);
+    case 15: return launch_grid_fused_t<7, 8, MODE, LB>(P, npolys, forced, st);
+    case 16: return launch_grid_fused_t<7, 9, MODE, LB>(P, npolys, forced, st);
+    case 17: return launch_grid_fused_t<7, 10, MODE, LB>(P, npolys, forced, st);
+  }
+  return fail(NTTMUL_EINVAL, "grid schedule: n = 2^%d unsupported", log_n);
+}
+
+// fused product: 0 = no, 1 = auto (may decline), 2 = forced
+inline int use_grid_fused(int log_n, long long npolys) {
+  if (log_n <= COL_LOG_R || log_n > 17 || g_split[log_n]) return 0;
+  const int s = g_sched_fused[log_n];
+  if (s == NTTMUL_SCHED_GRID) return 2;
+  static const int auto_max = std::getenv("NTTB_GRID_FUSED_MAX")
+                                  ? std::atoi(std::getenv("NTTB_GRID_FUSED_MAX"))
+                                  : 4;
+  return s == NTTMUL_SCHED_AUTO && npolys <= auto_max ? 1 : 0;
+}
+
 // Auto: up to 4 polynomials per call (grid sweep r2, grid_default_r2 /
 // grid_batch_r2.jsonl: one 2^16 ntt 8.1-9.3 -> 6.3 us, intt 8.6 -> 6.4 us;
 // two 2^16 11.0 -> 6.8 us, four 11.6 -> 9.0 us; 2^14 x 4 even, x 8 slower);
@@ -622,6 +686,13 @@ int run_polymul_m(u64 *c, const u64 *a, const u64 *b, u64 *ws, const TwSet &tw,
     if (!(phases & 2)) return NTTMUL_OK;
     RowParams R{c, a, b, tw, ls, 0, FIN_SCALED_SKIP, 0};
     return launch_row_fused<MODE, LB>(log_r, R, npolys, st);
+  }
+  if (phases == 7) {
+    if (const int g = use_grid_fused(log_n, npolys)) {
+      GridFusedParams P{c, a, b, ws, tw, ls, nullptr};
+      const int s = launch_grid_fused<MODE, LB>(log_n, P, npolys, g == 2, st);
+      if (s != NTTB_DECLINED) return s;
+    }
   }
   if constexpr (MODE == NTTMUL_RED_ONE_SUB && LB >= 16) {  // the proposed / dhem
     // constants with every modulus < 2^60 (the BASELINE bases)
@@ -1182,7 +1253,7 @@ int nttmul_set_split(int log_n, int log_r) {
 int nttmul_set_schedule(int which, int log_n, int schedule) {
   if (which < 0 || which > 1 || log_n < COL_LOG_R + 1 || log_n > NTTMUL_MAX_LOG_N ||
       schedule < NTTMUL_SCHED_AUTO || schedule > NTTMUL_SCHED_GRID ||
-      (schedule >= NTTMUL_SCHED_PASSES && which == 0) ||
+      (schedule == NTTMUL_SCHED_PASSES && which == 0) ||
       (schedule == NTTMUL_SCHED_CLUSTER && log_n > COL_LOG_R + 4))
     return fail(NTTMUL_EINVAL, "set_schedule(%d, %d, %d)", which, log_n, schedule);
   (which == 0 ? g_sched_fused : g_sched_xform)[log_n] = schedule;

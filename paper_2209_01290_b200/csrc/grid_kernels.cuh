@@ -96,13 +96,14 @@ constexpr size_t grid_smem_bytes() {
 // One pass of R stages starting at stage S0 of a 2^B-element transform
 // spread over the CTA: units of 2^R elements spaced 2^LK apart (the
 // radix.cuh unit), UNITS / T per thread.  Element o lives at GridGeom::idx(o)
-// in shared memory or, for FROM_G / TO_G, at gaddr(o) in global memory.
+// in shared memory or, for FROM_G / TO_G, at gaddr(o) in global memory
+// (read from gin, written to gout).
 // Forward passes stop after TS stages (truncated transforms); inverse
 // passes run stages TS-1 .. 0, the last with inv_stage0 when STAGE0 (global
 // stage 0, FinalMode fin).  CANON: canonicalise the forward output.
 template <int LB, int A, int B, int LOG_E, int S0, int R, bool INV, bool FROM_G, bool TO_G, int TS,
           bool STAGE0, bool CANON, class GA>
-__device__ __forceinline__ void grid_pass(u64 *__restrict__ sm, u64 *__restrict__ g, GA gaddr,
+__device__ __forceinline__ void grid_pass(u64 *__restrict__ sm, const u64 *gin, u64 *gout, GA gaddr,
                                           const ulonglong2 *__restrict__ tw, const Limb &L,
                                           const Mod &M, int fin) {
   using G = GridGeom<A, B, LOG_E>;
@@ -118,7 +119,7 @@ __device__ __forceinline__ void grid_pass(u64 *__restrict__ sm, u64 *__restrict_
 #pragma unroll
     for (int e = 0; e < (1 << R); ++e) {
       const int o = o0 + (e << LK);
-      x[0][e] = FROM_G ? g[gaddr(o)] : sm[G::idx(o)];
+      x[0][e] = FROM_G ? gin[gaddr(o)] : sm[G::idx(o)];
     }
     const u64 B0 = (1ULL << S0) + static_cast<u64>(grp);
     if constexpr (!INV) {
@@ -137,7 +138,7 @@ __device__ __forceinline__ void grid_pass(u64 *__restrict__ sm, u64 *__restrict_
     for (int e = 0; e < (1 << R); ++e) {
       const int o = o0 + (e << LK);
       if (TO_G)
-        g[gaddr(o)] = x[0][e];
+        gout[gaddr(o)] = x[0][e];
       else
         sm[G::idx(o)] = x[0][e];
     }
@@ -151,8 +152,9 @@ __device__ __forceinline__ void grid_pass(u64 *__restrict__ sm, u64 *__restrict_
 // twiddle tw[2^s + group] of the global table), and consecutive units
 // step over the columns first, so warps touch contiguous W-word segments.
 template <int LB, int A, int B, int LOG_E, bool INV, int I>
-__device__ __forceinline__ void grid_cols(u64 *sm, u64 *g, int c0, const ulonglong2 *tw,
-                                          const Limb &L, const Mod &M, int fin) {
+__device__ __forceinline__ void grid_cols(u64 *sm, const u64 *gin, u64 *gout, int c0,
+                                          const ulonglong2 *tw, const Limb &L, const Mod &M,
+                                          int fin) {
   using P = typename GridGeom<A, B, LOG_E>::template Plan<A>;
   constexpr int NP = P::NPASS;
   if constexpr (I >= 0 && I < NP) {
@@ -162,14 +164,14 @@ __device__ __forceinline__ void grid_cols(u64 *sm, u64 *g, int c0, const ulonglo
     };
     if constexpr (!INV) {
       grid_pass<LB, A, B, LOG_E, S0, R, false, I == 0, I == NP - 1, R, false, false>(
-          sm, g, gaddr, tw, L, M, fin);
+          sm, gin, gout, gaddr, tw, L, M, fin);
       if constexpr (I + 1 < NP) __syncthreads();
-      grid_cols<LB, A, B, LOG_E, false, I + 1>(sm, g, c0, tw, L, M, fin);
+      grid_cols<LB, A, B, LOG_E, false, I + 1>(sm, gin, gout, c0, tw, L, M, fin);
     } else {
       grid_pass<LB, A, B, LOG_E, S0, R, true, I == NP - 1, I == 0, R, I == 0, false>(
-          sm, g, gaddr, tw, L, M, fin);
+          sm, gin, gout, gaddr, tw, L, M, fin);
       if constexpr (I > 0) __syncthreads();
-      grid_cols<LB, A, B, LOG_E, true, I - 1>(sm, g, c0, tw, L, M, fin);
+      grid_cols<LB, A, B, LOG_E, true, I - 1>(sm, gin, gout, c0, tw, L, M, fin);
     }
   }
 }
@@ -191,13 +193,13 @@ __device__ __forceinline__ void grid_row(u64 *sm, u64 *row, const ulonglong2 *st
     if constexpr (!INV) {
       constexpr int TS = (TOP && KIND == FWD_TRUNC) ? R - 1 : R;
       grid_pass<LB, A, B, LOG_E, S0, R, false, I == 0, I == NP - 1, TS, false, I == NP - 1>(
-          sm, row, gaddr, stw, L, M, FIN_LAZY);
+          sm, row, row, gaddr, stw, L, M, FIN_LAZY);
       if constexpr (I + 1 < NP) __syncthreads();
       grid_row<LB, A, B, LOG_E, false, KIND, I + 1>(sm, row, stw, L, M);
     } else {
       constexpr int TS = (TOP && KIND == INV_SKIP) ? R - 1 : R;
       grid_pass<LB, A, B, LOG_E, S0, R, true, I == NP - 1, I == 0, TS, false, false>(
-          sm, row, gaddr, stw, L, M, FIN_LAZY);
+          sm, row, row, gaddr, stw, L, M, FIN_LAZY);
       if constexpr (I > 0) __syncthreads();
       grid_row<LB, A, B, LOG_E, true, KIND, I - 1>(sm, row, stw, L, M);
     }
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(GridGeom<A, B, LOG_E>::T) grid_kernel(const Gr
   constexpr int NPC = G::template Plan<A>::NPASS;
   constexpr int NPR = G::template Plan<B>::NPASS;
   if constexpr (!INV) {
-    grid_cols<LB, A, B, LOG_E, false, 0>(sm, a, r * G::W, tw, L, M, FIN_LAZY);
+    grid_cols<LB, A, B, LOG_E, false, 0>(sm, a, a, r * G::W, tw, L, M, FIN_LAZY);
     cp_async_wait<0>();
     grid_sync();  // (includes the CTA barrier that publishes stw)
     grid_row<LB, A, B, LOG_E, false, KIND, 0>(sm, row, stw, L, M);
@@ -248,8 +250,136 @@ __global__ void __launch_bounds__(GridGeom<A, B, LOG_E>::T) grid_kernel(const Gr
     __syncthreads();
     grid_row<LB, A, B, LOG_E, true, KIND, NPR - 1>(sm, row, stw, L, M);
     grid_sync();
-    grid_cols<LB, A, B, LOG_E, true, NPC - 1>(sm, a, r * G::W, tw, L, M, P.fin);
+    grid_cols<LB, A, B, LOG_E, true, NPC - 1>(sm, a, a, r * G::W, tw, L, M, P.fin);
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Fused product in one launch (polymul_fused of up to a few limb-products):
+// column phase of a -> c and b -> ws (the A truncated-transform column
+// stages), grid barrier, row phase (row stages 0 .. B-2 of a and b, the
+// Karatsuba middle on consecutive pairs, inverse row stages B-2 .. 0),
+// grid barrier, inverse column phase of c with the 2^-(log n - 1) scale.
+// The stages, the middle (fused_pair / fused_pair_lazy per reduction MODE)
+// and the lazy ranges are those of the row kernel's fused tail, so results
+// are bit-identical to the three-launch schedule (reference
+// polymul_fused / _kernels.pyx fused_middle, paper Alg. 8).
+
+struct GridFusedParams {
+  u64 *c;
+  const u64 *a;
+  const u64 *b;
+  u64 *ws;
+  TwSet tw;
+  LimbSet limbs;
+  unsigned *barrier;
+};
+
+template <int A, int B>
+constexpr size_t grid_fused_smem_bytes() {
+  return 2 * GridGeom<A, B, 1>::PADN * sizeof(u64) + 2 * (size_t(1) << B) * sizeof(ulonglong2);
+}
+
+// forward row stages [I, N) of a and b (one stage per pass; the first
+// reads the rows from global memory)
+template <int LB, int A, int B, int I, int N>
+__device__ __forceinline__ void grid_fused_fwd(u64 *sa, u64 *sb, const u64 *ga, const u64 *gb,
+                                               const ulonglong2 *stw, const Limb &L,
+                                               const Mod &M) {
+  if constexpr (I < N) {
+    auto gaddr = [](int o) { return static_cast<long long>(o); };
+    grid_pass<LB, A, B, 1, I, 1, false, I == 0, false, 1, false, false>(sa, ga, nullptr, gaddr,
+                                                                        stw, L, M, FIN_LAZY);
+    grid_pass<LB, A, B, 1, I, 1, false, I == 0, false, 1, false, false>(sb, gb, nullptr, gaddr,
+                                                                        stw, L, M, FIN_LAZY);
+    __syncthreads();
+    grid_fused_fwd<LB, A, B, I + 1, N>(sa, sb, ga, gb, stw, L, M);
+  }
+}
+
+// inverse row stages I .. 0 of c (the last writes the row to global, lazy)
+template <int LB, int A, int B, int I>
+__device__ __forceinline__ void grid_fused_inv(u64 *sc, u64 *gc, const ulonglong2 *stw,
+                                               const Limb &L, const Mod &M) {
+  if constexpr (I >= 0) {
+    auto gaddr = [](int o) { return static_cast<long long>(o); };
+    grid_pass<LB, A, B, 1, I, 1, true, false, I == 0, 1, false, false>(sc, nullptr, gc, gaddr,
+                                                                      stw, L, M, FIN_LAZY);
+    if constexpr (I > 0) __syncthreads();
+    grid_fused_inv<LB, A, B, I - 1>(sc, gc, stw, L, M);
+  }
+}
+
+// (register budget for 1024 resident threads per SM: 64 per thread, so
+// up to 4 limb-products of 2^16 / 2 of 2^17 fit co-resident in one launch)
+template <int A, int B>
+constexpr int grid_fused_minb() {
+  return GridGeom<A, B, 1>::T >= 1024 ? 1 : 1024 / GridGeom<A, B, 1>::T;
+}
+
+template <int A, int B, int MODE, int LB>
+__global__ void __launch_bounds__(GridGeom<A, B, 1>::T, (grid_fused_minb<A, B>()))
+    grid_fused_kernel(const GridFusedParams P) {
+  using G = GridGeom<A, B, 1>;
+  static_assert(A >= 1 && B >= A && B >= 2, "fused grid geometry");
+  // lazy Barrett middle (proposed / dhem constants, all moduli < 2^60), as
+  // in the row kernel's fused tail
+  constexpr bool LAZY_MID = NTTB_LAZY_MID && MODE == NTTMUL_RED_ONE_SUB && LB >= 16;
+  constexpr bool FAST = LAZY_MID && LB >= 32;
+  extern __shared__ u64 sm[];
+  u64 *sa = sm;
+  u64 *sb = sm + G::PADN;
+  ulonglong2 *stf = reinterpret_cast<ulonglong2 *>(sm + 2 * G::PADN);
+  ulonglong2 *sti = stf + (1 << B);
+  const long long poly = blockIdx.x >> A;
+  const int r = static_cast<int>(blockIdx.x & ((1u << A) - 1));
+  int limb;
+  const Limb &L = *limb_ptr(P.limbs, poly, limb);
+  const Mod M = mod_for<LB>(L.q);
+  const ulonglong2 *twf = P.tw.fwd + limb * P.tw.stride;
+  const ulonglong2 *twi = P.tw.inv + limb * P.tw.stride;
+  const long long off = poly << (A + B);
+  const long long roff = off + (static_cast<long long>(r) << B);
+  const u64 rowbase = (1ULL << A) + r;
+  for (int i = threadIdx.x; i < (1 << B); i += G::T) {  // the row's twiddles
+    if (i == 0) continue;
+    const int s = 31 - __clz(i);
+    const u64 j = (rowbase << s) + (i - (1 << s));
+    cp_async16(stf + i, twf + j);
+    cp_async16(sti + i, twi + j);
+  }
+  cp_async_commit();
+  // column phase: a -> c, b -> ws
+  grid_cols<LB, A, B, 1, false, 0>(sa, P.a + off, P.c + off, r * G::W, twf, L, M, FIN_LAZY);
+  grid_cols<LB, A, B, 1, false, 0>(sb, P.b + off, P.ws + off, r * G::W, twf, L, M, FIN_LAZY);
+  cp_async_wait<0>();
+  slot_barrier(P.barrier);
+  // row phase
+  grid_fused_fwd<LB, A, B, 0, B - 1>(sa, sb, P.c + roff, P.ws + roff, stf, L, M);
+  {
+    const int q = threadIdx.x;  // pair (2q, 2q + 1); T = 2^(B-1) pairs
+    const u64 a0 = sa[G::idx(2 * q)], a1 = sa[G::idx(2 * q + 1)];
+    const u64 b0 = sb[G::idx(2 * q)], b1 = sb[G::idx(2 * q + 1)];
+    // twiddle of the row-local stage B-2 group of the pair; sign of the z
+    // term = parity of the global pair index = parity of q
+    const ulonglong2 w = stf[(1 << (B - 2)) + (q >> 1)];
+    u64 c0, c1;
+    if constexpr (LAZY_MID)
+      fused_pair_lazy<FAST>(to2q_any<LB>(a0, M), to2q_any<LB>(a1, M), to2q_any<LB>(b0, M),
+                            to2q_any<LB>(b1, M), w.x, w.y, (q & 1) != 0, L, M, c0, c1);
+    else
+      fused_pair<MODE>(canon_fwd<LB>(a0, M), canon_fwd<LB>(a1, M), canon_fwd<LB>(b0, M),
+                       canon_fwd<LB>(b1, M), w.x, w.y, (q & 1) != 0, L, M, c0, c1);
+    sa[G::idx(2 * q)] = c0;
+    sa[G::idx(2 * q + 1)] = c1;
+  }
+  __syncthreads();
+  grid_fused_inv<LB, A, B, B - 2>(sa, P.c + roff, sti, L, M);
+  slot_barrier(P.barrier);
+  grid_cols<LB, A, B, 1, true, G::template Plan<A>::NPASS - 1>(sa, P.c + off, P.c + off,
+                                                                 r * G::W, twi, L, M,
+                                                                 FIN_SCALED_SKIP);
 }
 
 }  // namespace nttb

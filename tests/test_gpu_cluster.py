@@ -106,7 +106,7 @@ def test_cluster_standalone_transforms(log_n):
 
 
 def test_schedule_knob_rejects_bad_arguments():
-    for args in ((2, 14, 1), (0, 12, 1), (0, 17, 2), (0, 14, 3), (0, 14, 4), (1, 14, 5),
+    for args in ((2, 14, 1), (0, 12, 1), (0, 17, 2), (0, 14, 3), (0, 14, 5), (1, 14, 5),
                  (1, 18, 1), (1, 17, 2)):
         with pytest.raises(nt._lib.NttmulError):
             lib.call("nttmul_set_schedule", *args)
@@ -272,3 +272,53 @@ def test_grid_schedule_rejects_oversized_batch():
     with schedule(1, 17, lib.SCHED_GRID):
         with pytest.raises(nt._lib.NttmulError):
             nt.kernels.ntt_ct(x, plan.tw_fwd, *plan.red_args, False, None)
+
+
+@pytest.mark.parametrize("variant", ["proposed", "classical", "builtin"])
+@pytest.mark.parametrize("bits", [40, 59, 61, 62])
+@pytest.mark.parametrize("log_n", [13, 14, 15, 16, 17])
+def test_grid_fused_product_bit_exact(log_n, bits, variant):
+    """The one-launch fused product (forward columns, rows + Karatsuba
+    middle, inverse columns) for every reduction variant and lazy-bound
+    class, forced on and in auto (up to 4 limb-products), against the
+    three-launch schedule and the oracle."""
+    n = 1 << log_n
+    # a forced grid launch must fit co-resident: 2 limb-products (one at
+    # 2^17, whose 512-thread CTAs run one per SM)
+    L, B = (1, 1) if log_n == 17 else (2, 1)
+    basis = nt.RnsBasis.build(n, bits, L, seed=1, variant=variant)
+    A = np.stack([np.stack([rand(q, n, 17 * b + l) for l, q in enumerate(basis.primes)])
+                  for b in range(B)])
+    Bm = np.stack([np.stack([rand(q, n, 404 + 17 * b + l) for l, q in enumerate(basis.primes)])
+                   for b in range(B)])
+    with schedule(0, log_n, lib.SCHED_THREE):
+        three = nt.polymul_rns_batch(dev(A), dev(Bm), basis).cpu().numpy()
+    with schedule(0, log_n, lib.SCHED_GRID):
+        got = nt.polymul_rns_batch(dev(A), dev(Bm), basis).cpu().numpy()
+    auto = nt.polymul_rns_batch(dev(A), dev(Bm), basis).cpu().numpy()
+    assert np.array_equal(got, three) and np.array_equal(auto, three)
+    want = oracle.polymul_rns(A, Bm, basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(got, want)
+
+
+def test_grid_fused_edge_values_and_aliasing():
+    """q - 1 everywhere, x^(n-1) * x = -1, and c aliasing a, through the
+    forced one-launch fused product."""
+    n = 1 << 16
+    basis = nt.RnsBasis.build(n, 60, 2, seed=0)
+    q = np.array(basis.primes, dtype=np.uint64)[None, :, None]
+    top = np.broadcast_to(q - 1, (1, 2, n)).copy()
+    X = np.zeros((1, 2, n), dtype=np.uint64)
+    Y = np.zeros((1, 2, n), dtype=np.uint64)
+    X[..., n - 1] = 1
+    Y[..., 1] = 1
+    with schedule(0, 16, lib.SCHED_GRID):
+        got = nt.polymul_rns_batch(dev(top), dev(top), basis).cpu().numpy()
+        wrap = nt.polymul_rns_batch(dev(X), dev(Y), basis).cpu().numpy()
+        da = dev(X)
+        nt.polymul_rns_batch(da, dev(Y), basis, out=da)
+        inplace = da.cpu().numpy()
+    want = oracle.polymul_rns(top, top, basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(got, want)
+    assert np.array_equal(wrap[..., 0], (q - 1)[..., 0]) and not wrap[..., 1:].any()
+    assert np.array_equal(inplace, wrap)
