@@ -489,6 +489,7 @@ def main():
     # ---- short device measurements while the GPU is still at full clock
     # (after the multi-second CPU baseline the clocks have dropped) ----
     ntt_us = ntt_latency_us(nt, basis.plans[0]) if rank == 0 else None
+    polymul_us = polymul_latency_us(nt, basis.plans[0]) if rank == 0 else None
     crt = crt_rates(nt, full, min(args.batch, 16)) if rank == 0 and mode == "ct" else None
     # ---- e2e: public API with host buffers, copies inside timing ----
     e2e = None
@@ -516,7 +517,7 @@ def main():
             "parity": {"checked": f"ciphertexts {chk} of every rank's shard vs the C oracle "
                                   "(reference restatement), before timing", "ok": True},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-            "ntt_us": ntt_us, "crt": crt,
+            "ntt_us": ntt_us, "polymul_us": polymul_us, "crt": crt,
             "gpu_launches": args.steps * (3 if log_n1 else 1) *
                             (2 if log_n1 and Bn * L >= 128 else 1),
             "clocks": clk.summary(), "impl": "ours",
@@ -776,6 +777,71 @@ def ntt_latency_us(nt, plan):
     e1.record(stream)
     torch.cuda.synchronize()
     res["api_us"] = round(e0.elapsed_time(e1) * 1e3 / 50, 2)
+    return res
+
+
+def polymul_latency_us(nt, plan):
+    """Latency of ONE fused limb-product (polymul_fused of one prime, the
+    one-launch grid schedule): device time per call from a CUDA graph of 20
+    back-to-back C-ABI calls, and per call through the Python API
+    (nt.polymul_fused on device tensors, 50 back-to-back calls, events)."""
+    import numpy as np
+    import torch
+
+    from paper_2209_01290_b200.polymul import mode_flags
+
+    fused = nt.FusedPlan.from_plan(plan)
+    n = plan.n
+    rng = np.random.default_rng(5)
+    a = torch.from_numpy(rng.integers(0, plan.q, n, dtype=np.uint64)).cuda()
+    b = torch.from_numpy(rng.integers(0, plan.q, n, dtype=np.uint64)).cuda()
+    c, ws = torch.empty_like(a), torch.empty_like(a)
+    limbs = plan.limb_device()
+    mode = mode_flags(plan.red_args[1], [plan.q])
+    log_n = n.bit_length() - 1
+    side = torch.cuda.Stream()
+
+    def launch(st):
+        nt._lib.call("nttmul_polymul_fused_rns", c.data_ptr(), a.data_ptr(), b.data_ptr(),
+                     limbs.data_ptr(), fused.fwd_pairs_half.data_ptr(),
+                     fused.inv_pairs_half.data_ptr(), log_n, 1, 1, mode, ws.data_ptr(), st)
+
+    res = {}
+    with torch.cuda.stream(side):
+        for _ in range(5):
+            launch(side.cuda_stream)
+        torch.cuda.synchronize()
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(20):
+                    launch(side.cuda_stream)
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(side)
+            for _ in range(10):
+                g.replay()
+            e1.record(side)
+            torch.cuda.synchronize()
+            res["device_us"] = round(e0.elapsed_time(e1) * 1e3 / 200, 2)
+        except Exception as exc:  # noqa: BLE001 - report, keep the API number
+            res["device_us"] = None
+            res["graph_error"] = str(exc)[:120]
+    ref = c.clone()
+    stream = torch.cuda.current_stream()
+    for _ in range(5):
+        out = nt.polymul_fused(a, b, fused)
+    torch.cuda.synchronize()
+    res["api_matches_c_abi"] = bool(torch.equal(out, ref))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(50):
+        nt.polymul_fused(a, b, fused)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    res["api_us"] = round(e0.elapsed_time(e1) * 1e3 / 50, 2)
+    res["n"] = n
     return res
 
 

@@ -58,6 +58,27 @@ class FusedPlan:
             plan._cache[key] = cached
         return cached
 
+    @property
+    def mode(self) -> int:
+        """C-ABI reduction mode with the lazy-bound flags of this prime."""
+        m = self.base._cache.get("fused_mode")
+        if m is None:
+            m = self.base._cache["fused_mode"] = mode_flags(self.base.red_args[1], [self.base.q])
+        return m
+
+    def workspace(self) -> torch.Tensor | None:
+        """Scratch of one limb-product for the column passes (n > 4096),
+        kept per device and stream: calls on one stream are ordered, so they
+        can share it (a fresh allocation per call costs host time)."""
+        if self.base.log_n <= 12:
+            return None
+        key = ("fused_ws", _device.index(), _device.stream_ptr())
+        ws = self.base._cache.get(key)
+        if ws is None:
+            ws = self.base._cache[key] = torch.empty(self.base.n, dtype=_device.U64,
+                                                     device=_device.device())
+        return ws
+
 
 def _coeffs(a, n: int):
     """(device tensor, came_from_device) of a normal-order operand."""
@@ -198,7 +219,7 @@ def run_fused(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, fwd_pairs, in
               limbs_dev: torch.Tensor, log_n: int, num_limbs: int, batch: int, mode: int,
               workspace: torch.Tensor | None = None) -> None:
     """Launch the fused RNS polymul over [batch, num_limbs, n] device tensors."""
-    if log_n > 10 and workspace is None:  # column passes need scratch (n > row length)
+    if log_n > 12 and workspace is None:  # column passes need scratch (n > row length)
         workspace = torch.empty_like(a)
     _lib.call("nttmul_polymul_fused_rns", out.data_ptr(), a.data_ptr(), b.data_ptr(),
               limbs_dev.data_ptr(), fwd_pairs.data_ptr(), inv_pairs.data_ptr(), log_n,
@@ -218,9 +239,8 @@ def polymul_fused(a, b, plan: NttPlan | FusedPlan, ctr: OpCounter | None = None)
     ta, dev_a = _coeffs(a, base.n)
     tb, dev_b = _coeffs(b, base.n)
     out = torch.empty_like(ta)
-    mode = mode_flags(base.red_args[1], [base.q])
     run_fused(out, ta, tb, fused.fwd_pairs_half, fused.inv_pairs_half, base.limb_device(),
-              base.log_n, 1, 1, mode)
+              base.log_n, 1, 1, fused.mode, fused.workspace())
     _finish(ctr, _fused_counts(base.n))
     return _result(out, dev_a or dev_b)
 
