@@ -87,10 +87,12 @@ struct GridGeom {
   };
 };
 
-// Shared-memory bytes of a grid kernel: the row (padded) + its twiddles.
+// Shared-memory bytes of a grid kernel: the row (padded), its twiddles and
+// the column twiddles.
 template <int A, int B, int LOG_E>
 constexpr size_t grid_smem_bytes() {
-  return GridGeom<A, B, LOG_E>::PADN * sizeof(u64) + (size_t(1) << B) * sizeof(ulonglong2);
+  return GridGeom<A, B, LOG_E>::PADN * sizeof(u64) +
+         ((size_t(1) << B) + (size_t(1) << A)) * sizeof(ulonglong2);
 }
 
 // One pass of R stages starting at stage S0 of a 2^B-element transform
@@ -151,7 +153,7 @@ __device__ __forceinline__ void grid_pass(u64 *__restrict__ sm, const u64 *gin, 
 // 0 .. A-1 of a 2^B-element transform (group of stage s = row >> (A - s),
 // twiddle tw[2^s + group] of the global table), and consecutive units
 // step over the columns first, so warps touch contiguous W-word segments.
-template <int LB, int A, int B, int LOG_E, bool INV, int I>
+template <int LB, int A, int B, int LOG_E, bool INV, int I, bool GIN = true>
 __device__ __forceinline__ void grid_cols(u64 *sm, const u64 *gin, u64 *gout, int c0,
                                           const ulonglong2 *tw, const Limb &L, const Mod &M,
                                           int fin) {
@@ -163,15 +165,15 @@ __device__ __forceinline__ void grid_cols(u64 *sm, const u64 *gin, u64 *gout, in
       return (static_cast<long long>(o >> (B - A)) << B) + c0 + (o & ((1 << (B - A)) - 1));
     };
     if constexpr (!INV) {
-      grid_pass<LB, A, B, LOG_E, S0, R, false, I == 0, I == NP - 1, R, false, false>(
+      grid_pass<LB, A, B, LOG_E, S0, R, false, GIN && I == 0, I == NP - 1, R, false, false>(
           sm, gin, gout, gaddr, tw, L, M, fin);
       if constexpr (I + 1 < NP) __syncthreads();
-      grid_cols<LB, A, B, LOG_E, false, I + 1>(sm, gin, gout, c0, tw, L, M, fin);
+      grid_cols<LB, A, B, LOG_E, false, I + 1, GIN>(sm, gin, gout, c0, tw, L, M, fin);
     } else {
-      grid_pass<LB, A, B, LOG_E, S0, R, true, I == NP - 1, I == 0, R, I == 0, false>(
+      grid_pass<LB, A, B, LOG_E, S0, R, true, GIN && I == NP - 1, I == 0, R, I == 0, false>(
           sm, gin, gout, gaddr, tw, L, M, fin);
       if constexpr (I > 0) __syncthreads();
-      grid_cols<LB, A, B, LOG_E, true, I - 1>(sm, gin, gout, c0, tw, L, M, fin);
+      grid_cols<LB, A, B, LOG_E, true, I - 1, GIN>(sm, gin, gout, c0, tw, L, M, fin);
     }
   }
 }
@@ -181,7 +183,7 @@ __device__ __forceinline__ void grid_cols(u64 *sm, const u64 *gin, u64 *gout, in
 // from row-local stage 0 (the first reads global, the last canonicalises
 // and writes global); inverse passes run downward (the first reads global,
 // the last writes global, lazy).
-template <int LB, int A, int B, int LOG_E, bool INV, int KIND, int I>
+template <int LB, int A, int B, int LOG_E, bool INV, int KIND, int I, bool GIN = true>
 __device__ __forceinline__ void grid_row(u64 *sm, u64 *row, const ulonglong2 *stw, const Limb &L,
                                          const Mod &M) {
   using P = typename GridGeom<A, B, LOG_E>::template Plan<B>;
@@ -192,16 +194,16 @@ __device__ __forceinline__ void grid_row(u64 *sm, u64 *row, const ulonglong2 *st
     auto gaddr = [](int o) { return static_cast<long long>(o); };
     if constexpr (!INV) {
       constexpr int TS = (TOP && KIND == FWD_TRUNC) ? R - 1 : R;
-      grid_pass<LB, A, B, LOG_E, S0, R, false, I == 0, I == NP - 1, TS, false, I == NP - 1>(
-          sm, row, row, gaddr, stw, L, M, FIN_LAZY);
+      grid_pass<LB, A, B, LOG_E, S0, R, false, GIN && I == 0, I == NP - 1, TS, false,
+                I == NP - 1>(sm, row, row, gaddr, stw, L, M, FIN_LAZY);
       if constexpr (I + 1 < NP) __syncthreads();
-      grid_row<LB, A, B, LOG_E, false, KIND, I + 1>(sm, row, stw, L, M);
+      grid_row<LB, A, B, LOG_E, false, KIND, I + 1, GIN>(sm, row, stw, L, M);
     } else {
       constexpr int TS = (TOP && KIND == INV_SKIP) ? R - 1 : R;
-      grid_pass<LB, A, B, LOG_E, S0, R, true, I == NP - 1, I == 0, TS, false, false>(
+      grid_pass<LB, A, B, LOG_E, S0, R, true, GIN && I == NP - 1, I == 0, TS, false, false>(
           sm, row, row, gaddr, stw, L, M, FIN_LAZY);
       if constexpr (I > 0) __syncthreads();
-      grid_row<LB, A, B, LOG_E, true, KIND, I - 1>(sm, row, stw, L, M);
+      grid_row<LB, A, B, LOG_E, true, KIND, I - 1, GIN>(sm, row, stw, L, M);
     }
   }
 }
@@ -221,15 +223,34 @@ __global__ void __launch_bounds__(GridGeom<A, B, LOG_E>::T) grid_kernel(const Gr
   u64 *a = P.a + (poly << (A + B));
   const u64 rowbase = (1ULL << A) + r;
   u64 *row = a + (static_cast<long long>(r) << B);
-  // The row's twiddles - tw[(rowbase << s) + g] at row-local stage s - are
-  // staged into shared memory at stw[(1 << s) + g] first (async; in the
-  // forward transform this overlaps the column phase), so the row passes
-  // wait on shared memory instead of an L2 round trip per pass.
+  // Everything the first phase needs is staged into shared memory by one
+  // batch of cp.async at kernel start - the column twiddles tw[1 .. 2^A)
+  // at ctw[i], the row's twiddles tw[(rowbase << s) + g] (row-local stage
+  // s) at stw[(1 << s) + g], and the first phase's data (forward: the CTA's
+  // column block; inverse: its row) - so the first phase waits one memory
+  // latency instead of one L2 round trip per pass, and every later pass
+  // reads twiddles from shared memory (the row passes index stw with base 1).
   ulonglong2 *stw = reinterpret_cast<ulonglong2 *>(sm + G::PADN);
+  ulonglong2 *ctw = stw + (1 << B);
   for (int i = threadIdx.x; i < (1 << B); i += G::T) {
     if (i == 0) continue;
     const int s = 31 - __clz(i);
     cp_async16(stw + i, tw + ((rowbase << s) + (i - (1 << s))));
+  }
+  for (int i = threadIdx.x + 1; i < (1 << A); i += G::T) cp_async16(ctw + i, tw + i);
+  if constexpr (!INV) {
+#pragma unroll
+    for (int w = 0; w < (1 << B) / G::T; ++w) {  // column block: o = row * W + col
+      const int o = threadIdx.x + w * G::T;
+      cp_async8(sm + G::idx(o), a + (static_cast<long long>(o >> (B - A)) << B) + r * G::W +
+                                    (o & (G::W - 1)));
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < (1 << B) / G::T; ++w) {
+      const int o = threadIdx.x + w * G::T;
+      cp_async8(sm + G::idx(o), row + o);
+    }
   }
   cp_async_commit();
   auto grid_sync = [&] {
@@ -240,17 +261,16 @@ __global__ void __launch_bounds__(GridGeom<A, B, LOG_E>::T) grid_kernel(const Gr
   };
   constexpr int NPC = G::template Plan<A>::NPASS;
   constexpr int NPR = G::template Plan<B>::NPASS;
+  cp_async_wait<0>();
+  __syncthreads();
   if constexpr (!INV) {
-    grid_cols<LB, A, B, LOG_E, false, 0>(sm, a, a, r * G::W, tw, L, M, FIN_LAZY);
-    cp_async_wait<0>();
-    grid_sync();  // (includes the CTA barrier that publishes stw)
+    grid_cols<LB, A, B, LOG_E, false, 0, false>(sm, a, a, r * G::W, ctw, L, M, FIN_LAZY);
+    grid_sync();
     grid_row<LB, A, B, LOG_E, false, KIND, 0>(sm, row, stw, L, M);
   } else {
-    cp_async_wait<0>();
-    __syncthreads();
-    grid_row<LB, A, B, LOG_E, true, KIND, NPR - 1>(sm, row, stw, L, M);
+    grid_row<LB, A, B, LOG_E, true, KIND, NPR - 1, false>(sm, row, stw, L, M);
     grid_sync();
-    grid_cols<LB, A, B, LOG_E, true, NPC - 1>(sm, a, a, r * G::W, tw, L, M, P.fin);
+    grid_cols<LB, A, B, LOG_E, true, NPC - 1>(sm, a, a, r * G::W, ctw, L, M, P.fin);
   }
 }
 
@@ -278,7 +298,8 @@ struct GridFusedParams {
 
 template <int A, int B>
 constexpr size_t grid_fused_smem_bytes() {
-  return 2 * GridGeom<A, B, 1>::PADN * sizeof(u64) + 2 * (size_t(1) << B) * sizeof(ulonglong2);
+  return 2 * GridGeom<A, B, 1>::PADN * sizeof(u64) +
+         2 * ((size_t(1) << B) + (size_t(1) << A)) * sizeof(ulonglong2);
 }
 
 // forward row stages [I, N) of a and b (one stage per pass; the first
@@ -332,6 +353,8 @@ __global__ void __launch_bounds__(GridGeom<A, B, 1>::T, (grid_fused_minb<A, B>()
   u64 *sb = sm + G::PADN;
   ulonglong2 *stf = reinterpret_cast<ulonglong2 *>(sm + 2 * G::PADN);
   ulonglong2 *sti = stf + (1 << B);
+  ulonglong2 *ctf = sti + (1 << B);  // column twiddles tw[1 .. 2^A)
+  ulonglong2 *cti = ctf + (1 << A);
   const long long poly = blockIdx.x >> A;
   const int r = static_cast<int>(blockIdx.x & ((1u << A) - 1));
   int limb;
@@ -342,18 +365,35 @@ __global__ void __launch_bounds__(GridGeom<A, B, 1>::T, (grid_fused_minb<A, B>()
   const long long off = poly << (A + B);
   const long long roff = off + (static_cast<long long>(r) << B);
   const u64 rowbase = (1ULL << A) + r;
-  for (int i = threadIdx.x; i < (1 << B); i += G::T) {  // the row's twiddles
+  // one batch of cp.async (as in grid_kernel): the row's forward / inverse
+  // twiddles, the column twiddles, and the CTA's column blocks of a and b
+  for (int i = threadIdx.x; i < (1 << B); i += G::T) {
     if (i == 0) continue;
     const int s = 31 - __clz(i);
     const u64 j = (rowbase << s) + (i - (1 << s));
     cp_async16(stf + i, twf + j);
     cp_async16(sti + i, twi + j);
   }
+  for (int i = threadIdx.x + 1; i < (1 << A); i += G::T) {
+    cp_async16(ctf + i, twf + i);
+    cp_async16(cti + i, twi + i);
+  }
+#pragma unroll
+  for (int w = 0; w < (1 << B) / G::T; ++w) {  // column blocks: o = row * W + col
+    const int o = threadIdx.x + w * G::T;
+    const long long go = off + (static_cast<long long>(o >> (B - A)) << B) + r * G::W +
+                         (o & (G::W - 1));
+    cp_async8(sa + G::idx(o), P.a + go);
+    cp_async8(sb + G::idx(o), P.b + go);
+  }
   cp_async_commit();
-  // column phase: a -> c, b -> ws
-  grid_cols<LB, A, B, 1, false, 0>(sa, P.a + off, P.c + off, r * G::W, twf, L, M, FIN_LAZY);
-  grid_cols<LB, A, B, 1, false, 0>(sb, P.b + off, P.ws + off, r * G::W, twf, L, M, FIN_LAZY);
   cp_async_wait<0>();
+  __syncthreads();
+  // column phase: a -> c, b -> ws
+  grid_cols<LB, A, B, 1, false, 0, false>(sa, P.a + off, P.c + off, r * G::W, ctf, L, M,
+                                          FIN_LAZY);
+  grid_cols<LB, A, B, 1, false, 0, false>(sb, P.b + off, P.ws + off, r * G::W, ctf, L, M,
+                                          FIN_LAZY);
   slot_barrier(P.barrier);
   // row phase
   grid_fused_fwd<LB, A, B, 0, B - 1>(sa, sb, P.c + roff, P.ws + roff, stf, L, M);
@@ -378,7 +418,7 @@ __global__ void __launch_bounds__(GridGeom<A, B, 1>::T, (grid_fused_minb<A, B>()
   grid_fused_inv<LB, A, B, B - 2>(sa, P.c + roff, sti, L, M);
   slot_barrier(P.barrier);
   grid_cols<LB, A, B, 1, true, G::template Plan<A>::NPASS - 1>(sa, P.c + off, P.c + off,
-                                                                 r * G::W, twi, L, M,
+                                                                 r * G::W, cti, L, M,
                                                                  FIN_SCALED_SKIP);
 }
 
