@@ -87,6 +87,22 @@ struct GridGeom {
   };
 };
 
+// Barrier between two passes (first stages S0a, S0b; Ra, Rb stages) of a
+// 2^B-element grid transform.  A pass of R == LOG_E stages gives each
+// thread one unit; when its groups span at most the 2^(5+LOG_E) elements of
+// a warp (B - S0 <= 5 + LOG_E), warp w's units cover exactly elements
+// [w 2^(5+LOG_E), (w+1) 2^(5+LOG_E)).  If both passes are like that, every
+// warp reads only what it wrote itself: a warp barrier suffices.
+template <int B, int LOG_E, int S0a, int Ra, int S0b, int Rb>
+__device__ __forceinline__ void pass_sync() {
+  constexpr bool WA = Ra == LOG_E && B - S0a <= 5 + LOG_E;
+  constexpr bool WB = Rb == LOG_E && B - S0b <= 5 + LOG_E;
+  if constexpr (WA && WB)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
 // Shared-memory bytes of a grid kernel: the row (padded), its twiddles and
 // the column twiddles.
 template <int A, int B, int LOG_E>
@@ -167,12 +183,12 @@ __device__ __forceinline__ void grid_cols(u64 *sm, const u64 *gin, u64 *gout, in
     if constexpr (!INV) {
       grid_pass<LB, A, B, LOG_E, S0, R, false, GIN && I == 0, I == NP - 1, R, false, false>(
           sm, gin, gout, gaddr, tw, L, M, fin);
-      if constexpr (I + 1 < NP) __syncthreads();
+      if constexpr (I + 1 < NP) pass_sync<B, LOG_E, S0, R, P::S0(I + 1), P::R(I + 1)>();
       grid_cols<LB, A, B, LOG_E, false, I + 1, GIN>(sm, gin, gout, c0, tw, L, M, fin);
     } else {
       grid_pass<LB, A, B, LOG_E, S0, R, true, GIN && I == NP - 1, I == 0, R, I == 0, false>(
           sm, gin, gout, gaddr, tw, L, M, fin);
-      if constexpr (I > 0) __syncthreads();
+      if constexpr (I > 0) pass_sync<B, LOG_E, S0, R, P::S0(I - 1), P::R(I - 1)>();
       grid_cols<LB, A, B, LOG_E, true, I - 1, GIN>(sm, gin, gout, c0, tw, L, M, fin);
     }
   }
@@ -196,13 +212,13 @@ __device__ __forceinline__ void grid_row(u64 *sm, u64 *row, const ulonglong2 *st
       constexpr int TS = (TOP && KIND == FWD_TRUNC) ? R - 1 : R;
       grid_pass<LB, A, B, LOG_E, S0, R, false, GIN && I == 0, I == NP - 1, TS, false,
                 I == NP - 1>(sm, row, row, gaddr, stw, L, M, FIN_LAZY);
-      if constexpr (I + 1 < NP) __syncthreads();
+      if constexpr (I + 1 < NP) pass_sync<B, LOG_E, S0, R, P::S0(I + 1), P::R(I + 1)>();
       grid_row<LB, A, B, LOG_E, false, KIND, I + 1, GIN>(sm, row, stw, L, M);
     } else {
       constexpr int TS = (TOP && KIND == INV_SKIP) ? R - 1 : R;
       grid_pass<LB, A, B, LOG_E, S0, R, true, GIN && I == NP - 1, I == 0, TS, false, false>(
           sm, row, row, gaddr, stw, L, M, FIN_LAZY);
-      if constexpr (I > 0) __syncthreads();
+      if constexpr (I > 0) pass_sync<B, LOG_E, S0, R, P::S0(I - 1), P::R(I - 1)>();
       grid_row<LB, A, B, LOG_E, true, KIND, I - 1, GIN>(sm, row, stw, L, M);
     }
   }
@@ -314,7 +330,7 @@ __device__ __forceinline__ void grid_fused_fwd(u64 *sa, u64 *sb, const u64 *ga, 
                                                                         stw, L, M, FIN_LAZY);
     grid_pass<LB, A, B, 1, I, 1, false, I == 0, false, 1, false, false>(sb, gb, nullptr, gaddr,
                                                                         stw, L, M, FIN_LAZY);
-    __syncthreads();
+    pass_sync<B, 1, I, 1, I + 1, 1>();  // (after the last: the middle, stage B-1 pairs)
     grid_fused_fwd<LB, A, B, I + 1, N>(sa, sb, ga, gb, stw, L, M);
   }
 }
@@ -327,7 +343,7 @@ __device__ __forceinline__ void grid_fused_inv(u64 *sc, u64 *gc, const ulonglong
     auto gaddr = [](int o) { return static_cast<long long>(o); };
     grid_pass<LB, A, B, 1, I, 1, true, false, I == 0, 1, false, false>(sc, nullptr, gc, gaddr,
                                                                       stw, L, M, FIN_LAZY);
-    if constexpr (I > 0) __syncthreads();
+    if constexpr (I > 0) pass_sync<B, 1, I, 1, I - 1, 1>();
     grid_fused_inv<LB, A, B, I - 1>(sc, gc, stw, L, M);
   }
 }
@@ -414,7 +430,7 @@ __global__ void __launch_bounds__(GridGeom<A, B, 1>::T, (grid_fused_minb<A, B>()
     sa[G::idx(2 * q)] = c0;
     sa[G::idx(2 * q + 1)] = c1;
   }
-  __syncthreads();
+  pass_sync<B, 1, B - 1, 1, B - 2, 1>();  // middle -> first inverse pass
   grid_fused_inv<LB, A, B, B - 2>(sa, P.c + roff, sti, L, M);
   slot_barrier(P.barrier);
   grid_cols<LB, A, B, 1, true, G::template Plan<A>::NPASS - 1>(sa, P.c + off, P.c + off,
