@@ -400,14 +400,13 @@ inline bool use_cluster(const int *table, int log_n, long long npolys) {
 // per thread and pass (grid_kernels.cuh).  Geometry per size from the grid
 // sweep (scripts/grid_sweep.py, profiles/r2/grid_sweep_r2.jsonl): one
 // element pair per thread (LOG_E = 1) up to 2^16, pairs of pairs at 2^17.
-// The grid barrier slot of the next launch (round-robin over GRID_SLOTS;
-// nullptr = cooperative launch + cooperative_groups grid sync, selected by
-// NTTB_GRID_COOP=1).
-int grid_barrier_slot(unsigned **slot) {
+// The grid barrier slot table of the current device (the launch picks its
+// slot from %gridid); nullptr = cooperative launch + cooperative_groups
+// grid sync, selected by NTTB_GRID_COOP=1.
+int grid_barrier_slot(unsigned **slots) {
   static const bool coop = std::getenv("NTTB_GRID_COOP") != nullptr;
-  *slot = nullptr;
+  *slots = nullptr;
   if (coop) return NTTMUL_OK;
-  static std::atomic<unsigned> ticket{0};
   thread_local unsigned *base[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cuda_status("device");
@@ -417,7 +416,7 @@ int grid_barrier_slot(unsigned **slot) {
       return cuda_status("grid barrier slots");
     base[dev] = static_cast<unsigned *>(p);
   }
-  *slot = base[dev] + ticket.fetch_add(1, std::memory_order_relaxed) % GRID_SLOTS;
+  *slots = base[dev];
   return NTTMUL_OK;
 }
 

@@ -36,21 +36,30 @@ struct GridParams {
   TwSet tw;
   LimbSet limbs;
   int fin;             // inverse: FinalMode of the global last stage
-  unsigned *barrier;   // the launch's grid barrier word (nullptr: cooperative launch)
+  unsigned *barrier;   // the grid barrier slot table (nullptr: cooperative launch)
 };
 
 // Grid barrier of a plain (non-cooperative) launch whose CTAs are all
 // co-resident (the host checks the grid against the occupancy): one
-// counter word per launch, in a slot the host hands out round-robin.  The
-// arrivals add up to exactly 2^31 (CTA 0 adds 2^31 - (n - 1), the others
-// 1), so the barrier is complete when bit 31 flips, and the word is left in
-// a valid state for its next user (a replay of the same graph, or the
-// launch that draws the slot GRID_SLOTS launches later) without a reset -
-// the flip-bit scheme of cooperative_groups' grid sync, minus the
-// cooperative launch, which costs ~2 us more per call when replayed from a
-// graph (scripts/microbench/launch_floor.cu).
-constexpr int GRID_SLOTS = 4096;
+// counter word per launch, the slot chosen by the launch itself from its
+// %gridid - the context's temporal launch number, distinct for every launch
+// including each replay of a captured graph - modulo GRID_SLOTS.  Two grid
+// launches share a word only if one still runs 2^18 kernel launches after
+// the other started.  The arrivals add up to exactly 2^31 (CTA 0 adds
+// 2^31 - (n - 1), the others 1), so the barrier is complete when bit 31
+// flips and the low bits return to their previous value (0): the word is
+// valid for its next user without a reset - the flip-bit scheme of
+// cooperative_groups' grid sync, minus the cooperative launch, which costs
+// ~2 us more per call when replayed from a graph
+// (scripts/microbench/launch_floor.cu).
+constexpr int GRID_SLOTS = 1 << 18;
 __device__ unsigned g_grid_barriers[GRID_SLOTS];
+
+__device__ __forceinline__ unsigned *launch_slot(unsigned *slots) {
+  unsigned long long id;
+  asm volatile("mov.u64 %0, %%gridid;" : "=l"(id));
+  return slots + (id & (GRID_SLOTS - 1));
+}
 
 __device__ __forceinline__ void slot_barrier(unsigned *bar) {
   __syncthreads();
@@ -271,7 +280,7 @@ __global__ void __launch_bounds__(GridGeom<A, B, LOG_E>::T) grid_kernel(const Gr
   cp_async_commit();
   auto grid_sync = [&] {
     if (P.barrier)
-      slot_barrier(P.barrier);
+      slot_barrier(launch_slot(P.barrier));
     else
       cooperative_groups::this_grid().sync();
   };
@@ -309,7 +318,7 @@ struct GridFusedParams {
   u64 *ws;
   TwSet tw;
   LimbSet limbs;
-  unsigned *barrier;
+  unsigned *barrier;  // the grid barrier slot table
 };
 
 template <int A, int B>
@@ -410,7 +419,7 @@ __global__ void __launch_bounds__(GridGeom<A, B, 1>::T, (grid_fused_minb<A, B>()
                                           FIN_LAZY);
   grid_cols<LB, A, B, 1, false, 0, false>(sb, P.b + off, P.ws + off, r * G::W, ctf, L, M,
                                           FIN_LAZY);
-  slot_barrier(P.barrier);
+  slot_barrier(launch_slot(P.barrier));
   // row phase
   grid_fused_fwd<LB, A, B, 0, B - 1>(sa, sb, P.c + roff, P.ws + roff, stf, L, M);
   {
@@ -432,7 +441,7 @@ __global__ void __launch_bounds__(GridGeom<A, B, 1>::T, (grid_fused_minb<A, B>()
   }
   pass_sync<B, 1, B - 1, 1, B - 2, 1>();  // middle -> first inverse pass
   grid_fused_inv<LB, A, B, B - 2>(sa, P.c + roff, sti, L, M);
-  slot_barrier(P.barrier);
+  slot_barrier(launch_slot(P.barrier));
   grid_cols<LB, A, B, 1, true, G::template Plan<A>::NPASS - 1>(sa, P.c + off, P.c + off,
                                                                  r * G::W, cti, L, M,
                                                                  FIN_SCALED_SKIP);

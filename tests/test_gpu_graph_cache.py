@@ -120,3 +120,49 @@ def test_fused_product_replays_and_user_capture():
     g.replay()
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_grid_launches_on_concurrent_streams():
+    """One-launch grid transforms and fused products issued from four
+    streams at once (each its own buffers, no host synchronisation), plus a
+    caller-captured CUDA graph of grid launches replayed concurrently: every
+    launch picks its own barrier word (csrc/grid_kernels.cuh launch_slot),
+    so all round trips come back exact."""
+    n = 1 << 15
+    plan = nt.build_plan(n, bits=60, seed=12)
+    fused = nt.FusedPlan.from_plan(plan)
+    inv_args = (plan.q, (plan.q + 1) // 2, *plan.red_args[1:], True, False, None)
+    bufs = [torch.from_numpy(rand(plan.q, n, 700 + i)[None]).cuda() for i in range(5)]
+    refs = [b.clone() for b in bufs]
+    prod_a = torch.from_numpy(rand(plan.q, n, 800)).cuda()
+    prod_b = torch.from_numpy(rand(plan.q, n, 801)).cuda()
+    want_prod = oracle.polymul_rns(rand(plan.q, n, 800)[None, None], rand(plan.q, n, 801)[None, None],
+                                   [plan.q], [plan.psi])[0, 0]
+    # a captured graph of forward + inverse on buffer 4
+    gstream = torch.cuda.Stream()
+    gstream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(gstream):
+        nt.kernels.ntt_ct(bufs[4], plan.tw_fwd, *plan.red_args, False, None)
+        nt.kernels.intt_gs(bufs[4], plan.tw_inv, *inv_args)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=gstream):
+        nt.kernels.ntt_ct(bufs[4], plan.tw_fwd, *plan.red_args, False, None)
+        nt.kernels.intt_gs(bufs[4], plan.tw_inv, *inv_args)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    prods = []
+    for it in range(25):
+        for i, s in enumerate(streams):
+            with torch.cuda.stream(s):
+                nt.kernels.ntt_ct(bufs[i], plan.tw_fwd, *plan.red_args, False, None)
+                nt.kernels.intt_gs(bufs[i], plan.tw_inv, *inv_args)
+                if i == 0 and it % 5 == 0:
+                    prods.append(nt.polymul_fused(prod_a, prod_b, fused))
+        with torch.cuda.stream(gstream):
+            g.replay()
+    torch.cuda.synchronize()
+    for i in range(5):
+        assert np.array_equal(bufs[i].cpu().numpy(), refs[i].cpu().numpy()), f"buffer {i}"
+    for p in prods:
+        assert np.array_equal(p.cpu().numpy(), want_prod)
