@@ -88,6 +88,9 @@ enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 #ifndef NTTB_LAZY_MID
 #define NTTB_LAZY_MID 1
 #endif
+#ifndef NTTB_ROW_TAIL_G
+#define NTTB_ROW_TAIL_G 1  // standalone rows: tail reads / writes global directly
+#endif
 
 template <int LOG_R, int LOG_E = NTTB_ROW_LOG_E>
 struct RowGeom {
@@ -426,6 +429,61 @@ __device__ __forceinline__ void tail_pass(u64 *__restrict__ sm, u64 rowbase,
   }
 }
 
+// Tail pass of a standalone (unfused) row reading its E consecutive words
+// straight from global memory (inverse rows: no staging copy + barrier in
+// front) or writing them straight back (forward rows: no barrier + copy
+// loop behind).  16-byte accesses when the row is 16-byte aligned.
+template <int LB, int LOG_R, int FWD, int INV, bool G_IN, bool G_OUT>
+__device__ __forceinline__ void tail_plain_g(u64 *__restrict__ sm, const u64 *gin, u64 *gout,
+                                             u64 rowbase, const ulonglong2 *__restrict__ twf,
+                                             const ulonglong2 *__restrict__ twi, const Mod &M) {
+  using G = RowGeom<LOG_R>;
+  constexpr int E = G::E;
+  constexpr int LE = G::HEAD == 0 ? 0 : LOG_R - G::HEAD;
+  const int o0 = threadIdx.x * E;
+  const u64 B0 = (rowbase << G::HEAD) + threadIdx.x;
+  const UnitIdx<LOG_R, 0> ix(o0);
+  u64 xa[1][E];
+  if constexpr (G_IN) {
+    if ((reinterpret_cast<uintptr_t>(gin) & 15) == 0) {
+      const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(gin + o0);
+#pragma unroll
+      for (int e = 0; e < E / 2; ++e) {
+        const ulonglong2 t = v[e];
+        xa[0][2 * e] = t.x;
+        xa[0][2 * e + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) xa[0][e] = gin[o0 + e];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) xa[0][e] = sm[ix(e)];
+  }
+  if (FWD == FWD_FULL) fwd_radix<LB, LE, LE, 1, G::HEAD & 1>(xa, B0, twf, M);
+  if (FWD == FWD_TRUNC) fwd_radix<LB, LE, LE - 1, 1, G::HEAD & 1>(xa, B0, twf, M);
+  if (INV == INV_FULL) inv_radix<LB, LE, LE, 0, 1>(xa, B0, twi, M);
+  if (INV == INV_SKIP) inv_radix<LB, LE, LE - 1, 0, 1>(xa, B0, twi, M);
+  if (INV == INV_NONE) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) xa[0][e] = canon_fwd<LB>(xa[0][e], M);
+  }
+  if constexpr (G_OUT) {
+    if ((reinterpret_cast<uintptr_t>(gout) & 15) == 0) {
+      ulonglong2 *v = reinterpret_cast<ulonglong2 *>(gout + o0);
+#pragma unroll
+      for (int e = 0; e < E / 2; ++e) v[e] = make_ulonglong2(xa[0][2 * e], xa[0][2 * e + 1]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) gout[o0 + e] = xa[0][e];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[ix(e)] = xa[0][e];
+  }
+}
+
 // Split CTA barrier (mbarrier): every thread arrives as soon as its writes
 // are done and waits only where it needs the other threads' data, so the
 // work placed between arrive and wait hides the barrier.
@@ -523,6 +581,20 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T, (row_minb<LOG_R, MID>()))
       for (int i = threadIdx.x; i < NP * LINES; i += G::T)
         discard_line((i < LINES ? P.in0 : P.in1) + off + (i % LINES) * 16);
     }
+  } else if constexpr (FWD != FWD_NONE && INV == INV_NONE && NTTB_ROW_TAIL_G) {
+    // standalone forward row: the tail writes the row straight to global
+    head_fwd_all<LB, LOG_R, NP>(sm, P.in0 + off, nullptr, rowbase, twf, M);
+    tail_plain_g<LB, LOG_R, FWD, INV, false, true>(sm, nullptr, P.out + off, rowbase, twf, twi,
+                                                   M);
+    return;
+  } else if constexpr (FWD == FWD_NONE && INV != INV_NONE && NTTB_ROW_TAIL_G) {
+    // standalone inverse row: the tail reads the row straight from global
+    tail_plain_g<LB, LOG_R, FWD, INV, true, false>(sm, P.in0 + off, nullptr, rowbase, twf, twi,
+                                                   M);
+    row_sync<LOG_R, G::S0(G::NPASS - 1)>();
+    head_inv_all<LB, LOG_R, G::NPASS - 1>(sm, P.out + off, rowbase, twi, L, M,
+                                          P.log_n1 == 0 ? P.fin : FIN_LAZY);
+    return;
   } else if (FWD != FWD_NONE) {
     head_fwd_all<LB, LOG_R, NP>(sm, P.in0 + off, nullptr, rowbase, twf, M);
   } else {
