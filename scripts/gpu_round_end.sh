@@ -14,3 +14,6 @@ timeout 600 python bench.py --log-n 17 --limbs 32 --batch 8 --no-cpu-baseline > 
 NTTB_BENCH_SHARE_GPU=1 timeout 600 python bench.py --gpus 2 --no-cpu-baseline > gpurun_out/re_bench_share2.json 2>&1
 timeout 600 python scripts/grid_sweep.py > gpurun_out/re_grid.jsonl 2>&1
 timeout 300 python scripts/host_overhead.py > gpurun_out/re_host_overhead.jsonl 2>&1
+timeout 600 python scripts/grid_fused_sweep.py > gpurun_out/re_grid_fused.jsonl 2>&1
+timeout 600 python scripts/api_timing.py > gpurun_out/re_api_timing.jsonl 2>&1
+timeout 900 python scripts/batched_xform.py > gpurun_out/re_batched.jsonl 2>&1
