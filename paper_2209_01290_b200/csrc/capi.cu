@@ -542,26 +542,48 @@ int launch_grid_fused(int log_n, const GridFusedParams &P, long long npolys, boo
 }
 
 // fused product: 0 = no, 1 = auto (may decline), 2 = forced
+// Auto limits per size (limb-products per call), from the grid sweeps
+// (profiles/r2/grid_fused_r2.jsonl, grid_fused_big_r2.jsonl): one launch vs
+// three, 2^13 x 32 products 34.6 -> 18.4 us, 2^14 x 8 26.8 -> 18.9 us (x 16
+// even), 2^15 x 8 35.9 -> 22.7 us, 2^16 x 4 36.9 -> 19.2 us; above the
+// co-resident CTA count the launcher declines (three launches).
+inline int grid_fused_auto_max(int log_n) {
+  switch (log_n) {
+    case 13: return 32;
+    case 14: return 8;
+    case 15: return 8;
+    case 16: return 4;
+    default: return 2;
+  }
+}
+
+// fused product: 0 = no, 1 = auto (may decline), 2 = forced
 inline int use_grid_fused(int log_n, long long npolys) {
   if (log_n <= COL_LOG_R || log_n > 17 || g_split[log_n]) return 0;
   const int s = g_sched_fused[log_n];
   if (s == NTTMUL_SCHED_GRID) return 2;
-  static const int auto_max = std::getenv("NTTB_GRID_FUSED_MAX")
-                                  ? std::atoi(std::getenv("NTTB_GRID_FUSED_MAX"))
-                                  : 4;
-  return s == NTTMUL_SCHED_AUTO && npolys <= auto_max ? 1 : 0;
+  return s == NTTMUL_SCHED_AUTO && npolys <= grid_fused_auto_max(log_n) ? 1 : 0;
 }
 
-// Auto: up to 4 polynomials per call (grid sweep r2, grid_default_r2 /
-// grid_batch_r2.jsonl: one 2^16 ntt 8.1-9.3 -> 6.3 us, intt 8.6 -> 6.4 us;
-// two 2^16 11.0 -> 6.8 us, four 11.6 -> 9.0 us; 2^14 x 4 even, x 8 slower);
-// larger batches keep the column / row kernels.  Every geometry holds
-// 4 x 2^A CTAs co-resident.
+// Auto limits for the standalone transforms (grid_default_r2 /
+// grid_batch_r2 / grid_big_r2.jsonl: one 2^16 ntt 8.1-9.3 -> 5.2 us; two
+// 2^16 11.0 -> 6.8 us, four 11.6 -> 9.0 us; 2^13 x 8 5.8 -> 4.7 us, 2^15 x 8
+// 12.6 -> 11.3 us; 2^14 x 4 even, x 8 7.9 -> 12.2 us); larger batches keep
+// the column / row kernels.  Every auto geometry holds its batch x 2^A CTAs
+// co-resident.
+inline int grid_auto_max(int log_n) {
+  switch (log_n) {
+    case 13: return 8;
+    case 15: return 8;
+    default: return 4;
+  }
+}
+
 inline bool use_grid(int log_n, long long npolys) {
   if (log_n <= COL_LOG_R || log_n > 17 || g_split[log_n]) return false;
   const int s = g_sched_xform[log_n];
   if (s == NTTMUL_SCHED_GRID) return true;
-  return s == NTTMUL_SCHED_AUTO && npolys <= 4;
+  return s == NTTMUL_SCHED_AUTO && npolys <= grid_auto_max(log_n);
 }
 
 constexpr int SMALL_MAX_LOG = 9;  // n <= 2^9 -> small kernel

@@ -322,3 +322,22 @@ def test_grid_fused_edge_values_and_aliasing():
     assert np.array_equal(got, want)
     assert np.array_equal(wrap[..., 0], (q - 1)[..., 0]) and not wrap[..., 1:].any()
     assert np.array_equal(inplace, wrap)
+
+
+@pytest.mark.parametrize("log_n,L,B", [(13, 8, 4), (14, 4, 2), (15, 8, 1)])
+def test_grid_fused_auto_larger_counts(log_n, L, B):
+    """Auto picks the one-launch fused product up to its per-size limit
+    (2^13: 32 limb-products, 2^14 / 2^15: 8): same result as three launches
+    and as the oracle."""
+    n = 1 << log_n
+    basis = nt.RnsBasis.build(n, 60, L, seed=2)
+    A = np.stack([np.stack([rand(q, n, 5 * b + l) for l, q in enumerate(basis.primes)])
+                  for b in range(B)])
+    Bm = np.stack([np.stack([rand(q, n, 55 + 5 * b + l) for l, q in enumerate(basis.primes)])
+                   for b in range(B)])
+    auto = nt.polymul_rns_batch(dev(A), dev(Bm), basis).cpu().numpy()
+    with schedule(0, log_n, lib.SCHED_THREE):
+        three = nt.polymul_rns_batch(dev(A), dev(Bm), basis).cpu().numpy()
+    assert np.array_equal(auto, three)
+    want = oracle.polymul_rns(A[:1], Bm[:1], basis.primes, [p.psi for p in basis.plans])
+    assert np.array_equal(auto[:1], want)
