@@ -78,8 +78,49 @@ def _remember(tw, q: int, entry) -> None:
 
 def register_pairs(tw: torch.Tensor, pairs: torch.Tensor, q: int, w1: int) -> None:
     """Record the pair table (and tw[1]) that belongs to device table ``tw``
-    (the caller - a plan - owns both; the cache holds no strong reference)."""
+    (the caller - a plan - owns both; the cache holds no strong reference).
+    The table is also attached to ``tw`` itself for the transforms' fast
+    path (``tw`` keeps its own pair table alive, nothing else)."""
     _remember(tw, q, (tw._version, weakref.ref(pairs), w1, None))
+    tw._nttb_pairs = (int(q), tw._version, pairs.data_ptr(), int(w1), pairs.shape[0], pairs)
+
+
+# ---------------------------------------------------------------------------
+# fast path of the transforms: a contiguous CUDA uint64 [n] / [batch, n]
+# operand and a plan's device twiddle table with its attached pair table.
+# Skips the general operand / cache machinery (a single transform's Python
+# overhead is otherwise larger than its device time); any other argument
+# takes the general path below, which also produces the errors.
+
+_FNS: dict = {}
+
+
+def _fn(name: str):
+    f = _FNS.get(name)
+    if f is None:
+        f = _FNS[name] = getattr(_lib.load(), name)
+    return f
+
+
+def _fast(a, tw, q):
+    """(data ptr, batch, log_n, pairs ptr, pair entries, w1) or None."""
+    if type(a) is not torch.Tensor or type(tw) is not torch.Tensor:
+        return None
+    e = tw.__dict__.get("_nttb_pairs")
+    if e is None or e[0] != q or e[1] != tw._version:
+        return None
+    if a.dtype is not _device.U64 or not a.is_cuda or not a.is_contiguous():
+        return None
+    sh = a.shape
+    if len(sh) == 1:
+        batch, n = 1, sh[0]
+    elif len(sh) == 2:
+        batch, n = sh
+    else:
+        return None
+    if n < 2 or n & (n - 1):
+        return None
+    return a.data_ptr(), batch, n.bit_length() - 1, e[2], e[4], e[3]
 
 
 def _lookup(tw, q: int):
@@ -109,6 +150,8 @@ def _pairs_for(tw, q: int):
     w1 = int(t[1].item()) if t.numel() > 1 else 1
     if isinstance(tw, torch.Tensor) and tw.is_cuda:
         _remember(tw, q, (tw._version, pairs, w1, None))
+        if pairs.device == tw.device:  # (the transforms' fast path)
+            tw._nttb_pairs = (q, tw._version, pairs.data_ptr(), w1, pairs.shape[0], pairs)
     elif isinstance(tw, np.ndarray):
         _remember(tw, q, (None, pairs, w1, np.array(tw, dtype=np.uint64, copy=True)))
     return pairs, w1
@@ -201,6 +244,13 @@ def _inv_counts(n: int, skip: bool):
 
 def ntt_ct(a, tw, q, mode, mu, s_in, s_out, truncate, counts=None):
     """Merged CT forward NTT in place (normal -> bit-reversed order)."""
+    f = _fast(a, tw, q) if counts is None else None
+    if f is not None and f[4] >= max((1 << f[2]) >> (1 if truncate else 0), 2):
+        st = _fn("nttmul_ntt_ct")(f[0], f[3], int(q), int(mode), int(mu), int(s_in), int(s_out),
+                                  1 if truncate else 0, f[2], f[1], _device.stream_ptr())
+        if st:
+            _lib.check(st, "nttmul_ntt_ct")
+        return
     op = _Operand(a, "a")
     batch, n = _shape(op)
     log_n = _log2(n)
@@ -218,6 +268,15 @@ def ntt_ct(a, tw, q, mode, mu, s_in, s_out, truncate, counts=None):
 
 def intt_gs(a, tw, q, half_q, mode, mu, s_in, s_out, scaled, skip_first, counts=None):
     """Merged GS inverse NTT in place (bit-reversed -> normal order)."""
+    f = _fast(a, tw, q) if counts is None else None
+    if f is not None and f[4] >= max((1 << f[2]) >> (1 if skip_first else 0), 2):
+        st = _fn("nttmul_intt_gs")(f[0], f[3], int(q), int(half_q), int(mode), int(mu),
+                                   int(s_in), int(s_out), 1 if scaled else 0,
+                                   1 if skip_first else 0, f[2], f[1], f[5],
+                                   _device.stream_ptr())
+        if st:
+            _lib.check(st, "nttmul_intt_gs")
+        return
     op = _Operand(a, "a")
     batch, n = _shape(op)
     log_n = _log2(n)

@@ -150,3 +150,30 @@ def test_concurrent_host_threads_on_split_path():
         t.join()
     assert not errors, errors
     assert all(np.array_equal(g, w) for g, w in zip(got, want))
+
+
+def test_transform_fast_path_tracks_twiddle_edits():
+    """The transforms' fast path (pair table attached to the plan's device
+    twiddle tensor) must notice an in-place edit of that tensor: after
+    overwriting tw_fwd with another prime's table the result follows the
+    new table, and restoring it restores the original result."""
+    n = 1 << 14
+    p1 = nt.build_plan(n, bits=60, seed=1)
+    x0 = rand(p1.q, n, 3)
+    f, _ = oracle.twiddles(p1.q, p1.psi, 14)
+    want = x0.copy()
+    oracle.ntt_ct(want, f, *p1.red_args, False)
+    x = torch.from_numpy(x0.copy()).cuda()
+    nt.kernels.ntt_ct(x, p1.tw_fwd, *p1.red_args, False, None)
+    assert np.array_equal(x.cpu().numpy(), want)
+    saved = p1.tw_fwd.clone()
+    p1.tw_fwd.copy_(p1.tw_inv)  # a different (inverse) table, same prime
+    other = x0.copy()
+    oracle.ntt_ct(other, p1.tw_inv.cpu().numpy(), *p1.red_args, False)
+    x = torch.from_numpy(x0.copy()).cuda()
+    nt.kernels.ntt_ct(x, p1.tw_fwd, *p1.red_args, False, None)
+    assert np.array_equal(x.cpu().numpy(), other)
+    p1.tw_fwd.copy_(saved)
+    x = torch.from_numpy(x0.copy()).cuda()
+    nt.kernels.ntt_ct(x, p1.tw_fwd, *p1.red_args, False, None)
+    assert np.array_equal(x.cpu().numpy(), want)
