@@ -226,6 +226,31 @@ def run_fused(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, fwd_pairs, in
               num_limbs, batch, mode, _device.ptr(workspace), _device.stream_ptr())
 
 
+def _fused_fast(a: torch.Tensor, b: torch.Tensor, fused: FusedPlan):
+    """One limb-product of contiguous CUDA uint64 [n] operands with the
+    plan's cached device pointers (a single product's Python overhead is
+    otherwise comparable to its device time); None -> the general path."""
+    base = fused.base
+    n = base.n
+    if (a.dtype is not _device.U64 or b.dtype is not _device.U64 or not a.is_cuda
+            or not b.is_cuda or a.shape != (n,) or b.shape != (n,)
+            or not a.is_contiguous() or not b.is_contiguous() or a.device != b.device):
+        return None
+    key = ("fused_fast", a.device.index)
+    c = base._cache.get(key)
+    if c is None:
+        c = base._cache[key] = (fused.fwd_pairs_half.data_ptr(), fused.inv_pairs_half.data_ptr(),
+                                base.limb_device().data_ptr(), fused.mode, base.log_n)
+    out = torch.empty_like(a)
+    ws = fused.workspace()
+    st = _lib.load().nttmul_polymul_fused_rns(
+        out.data_ptr(), a.data_ptr(), b.data_ptr(), c[2], c[0], c[1], c[4], 1, 1, c[3],
+        0 if ws is None else ws.data_ptr(), _device.stream_ptr())
+    if st:
+        _lib.check(st, "nttmul_polymul_fused_rns")
+    return out
+
+
 def polymul_fused(a, b, plan: NttPlan | FusedPlan, ctr: OpCounter | None = None):
     """Negacyclic product through the fused pipeline (one GPU call).
 
@@ -236,6 +261,10 @@ def polymul_fused(a, b, plan: NttPlan | FusedPlan, ctr: OpCounter | None = None)
     base = fused.base
     if base.n < 4:
         return polymul_ntt(a, b, base, ctr)
+    if ctr is None and type(a) is torch.Tensor and type(b) is torch.Tensor:
+        out = _fused_fast(a, b, fused)
+        if out is not None:
+            return out
     ta, dev_a = _coeffs(a, base.n)
     tb, dev_b = _coeffs(b, base.n)
     out = torch.empty_like(ta)
