@@ -420,8 +420,13 @@ int grid_barrier_slot(unsigned **slots) {
   return NTTMUL_OK;
 }
 
+// A grid launch that would not fit co-resident: an error when the schedule
+// was forced (NTTMUL_SCHED_GRID), else NTTB_DECLINED and the caller falls
+// back to the multi-launch schedule.
+constexpr int NTTB_DECLINED = -1;
+
 template <int A, int B, int LOG_E, bool INV, int KIND, int LB>
-int launch_grid_t(GridParams P, long long npolys, cudaStream_t st) {
+int launch_grid_t(GridParams P, long long npolys, bool forced, cudaStream_t st) {
   using G = GridGeom<A, B, LOG_E>;
   const size_t smem = grid_smem_bytes<A, B, LOG_E>();
   auto k = grid_kernel<A, B, LOG_E, INV, KIND, LB>;
@@ -437,9 +442,11 @@ int launch_grid_t(GridParams P, long long npolys, cudaStream_t st) {
     cap.store(per_sm * sms);
   }
   const long long blocks = npolys << A;
-  if (blocks > cap.load())
+  if (blocks > cap.load()) {
+    if (!forced) return NTTB_DECLINED;
     return fail(NTTMUL_EINVAL, "grid schedule: %lld CTAs exceed the %d co-resident", blocks,
                 cap.load());
+  }
   CHECK(grid_barrier_slot(&P.barrier));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(blocks));
@@ -460,14 +467,14 @@ int launch_grid_t(GridParams P, long long npolys, cudaStream_t st) {
 // (< 2^60 moduli) and inverse kernels of every (A, LOG_E) of the sweep are
 // instantiated too and NTTB_GRID_A / NTTB_GRID_E select one.
 template <bool INV, int KIND, int LB>
-int launch_grid(int log_n, const GridParams &P, long long npolys, cudaStream_t st) {
+int launch_grid(int log_n, const GridParams &P, long long npolys, bool forced, cudaStream_t st) {
 #ifdef NTTB_GRID_SWEEP
   if constexpr ((!INV && LB == 16 && KIND == FWD_FULL) || (INV && LB == 8 && KIND == INV_FULL)) {
     static const int A = std::getenv("NTTB_GRID_A") ? std::atoi(std::getenv("NTTB_GRID_A")) : 0;
     static const int E = std::getenv("NTTB_GRID_E") ? std::atoi(std::getenv("NTTB_GRID_E")) : 0;
 #define NTTB_G(LN, AV, EV)                \
   if (log_n == LN && A == AV && E == EV) \
-    return launch_grid_t<AV, LN - AV, EV, INV, KIND, LB>(P, npolys, st);
+    return launch_grid_t<AV, LN - AV, EV, INV, KIND, LB>(P, npolys, forced, st);
 #define NTTB_GE(LN, AV) NTTB_G(LN, AV, 1) NTTB_G(LN, AV, 2) NTTB_G(LN, AV, 3)
     NTTB_GE(13, 5) NTTB_GE(13, 6)
     NTTB_GE(14, 6) NTTB_GE(14, 7)
@@ -479,11 +486,11 @@ int launch_grid(int log_n, const GridParams &P, long long npolys, cudaStream_t s
   }
 #endif
   switch (log_n) {
-    case 13: return launch_grid_t<5, 8, 1, INV, KIND, LB>(P, npolys, st);
-    case 14: return launch_grid_t<7, 7, 1, INV, KIND, LB>(P, npolys, st);
-    case 15: return launch_grid_t<7, 8, 1, INV, KIND, LB>(P, npolys, st);
-    case 16: return launch_grid_t<7, 9, 1, INV, KIND, LB>(P, npolys, st);
-    case 17: return launch_grid_t<7, 10, 2, INV, KIND, LB>(P, npolys, st);
+    case 13: return launch_grid_t<5, 8, 1, INV, KIND, LB>(P, npolys, forced, st);
+    case 14: return launch_grid_t<7, 7, 1, INV, KIND, LB>(P, npolys, forced, st);
+    case 15: return launch_grid_t<7, 8, 1, INV, KIND, LB>(P, npolys, forced, st);
+    case 16: return launch_grid_t<7, 9, 1, INV, KIND, LB>(P, npolys, forced, st);
+    case 17: return launch_grid_t<7, 10, 2, INV, KIND, LB>(P, npolys, forced, st);
   }
   return fail(NTTMUL_EINVAL, "grid schedule: n = 2^%d unsupported", log_n);
 }
@@ -492,7 +499,6 @@ int launch_grid(int log_n, const GridParams &P, long long npolys, cudaStream_t s
 // standalone grid schedule, one element pair per thread.  Returns
 // NTTB_DECLINED when the launch would not fit co-resident and the schedule
 // was not forced.
-constexpr int NTTB_DECLINED = -1;
 
 template <int A, int B, int MODE, int LB>
 int launch_grid_fused_t(GridFusedParams P, long long npolys, bool forced, cudaStream_t st) {
@@ -579,11 +585,12 @@ inline int grid_auto_max(int log_n) {
   }
 }
 
-inline bool use_grid(int log_n, long long npolys) {
-  if (log_n <= COL_LOG_R || log_n > 17 || g_split[log_n]) return false;
+// 0 = no, 1 = auto (may decline), 2 = forced
+inline int use_grid(int log_n, long long npolys) {
+  if (log_n <= COL_LOG_R || log_n > 17 || g_split[log_n]) return 0;
   const int s = g_sched_xform[log_n];
-  if (s == NTTMUL_SCHED_GRID) return true;
-  return s == NTTMUL_SCHED_AUTO && npolys <= grid_auto_max(log_n);
+  if (s == NTTMUL_SCHED_GRID) return 2;
+  return s == NTTMUL_SCHED_AUTO && npolys <= grid_auto_max(log_n) ? 1 : 0;
 }
 
 constexpr int SMALL_MAX_LOG = 9;  // n <= 2^9 -> small kernel
@@ -607,10 +614,11 @@ int run_forward(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
       return launch_cluster<CL_FWD, 2, LB>(log_n - COL_LOG_R, P, npolys, st);
     }
   }
-  if (use_grid(log_n, npolys)) {
+  if (const int g = use_grid(log_n, npolys)) {
     GridParams P{a, tw, ls, FIN_PLAIN, nullptr};
-    return truncate ? launch_grid<false, FWD_TRUNC, LB>(log_n, P, npolys, st)
-                    : launch_grid<false, FWD_FULL, LB>(log_n, P, npolys, st);
+    const int s = truncate ? launch_grid<false, FWD_TRUNC, LB>(log_n, P, npolys, g == 2, st)
+                           : launch_grid<false, FWD_FULL, LB>(log_n, P, npolys, g == 2, st);
+    if (s != NTTB_DECLINED) return s;
   }
   if (use_passes(log_n, npolys, false)) {
     const int LAT_LOG_R = lat_log_r(log_n);
@@ -652,10 +660,11 @@ int run_inverse(u64 *a, const TwSet &tw, const LimbSet &ls, int log_n,
       return launch_cluster<CL_INV, 2, LB>(log_n - COL_LOG_R, P, npolys, st);
     }
   }
-  if (use_grid(log_n, npolys)) {
+  if (const int g = use_grid(log_n, npolys)) {
     GridParams P{a, tw, ls, fin, nullptr};
-    return skip ? launch_grid<true, INV_SKIP, LB>(log_n, P, npolys, st)
-                : launch_grid<true, INV_FULL, LB>(log_n, P, npolys, st);
+    const int s = skip ? launch_grid<true, INV_SKIP, LB>(log_n, P, npolys, g == 2, st)
+                       : launch_grid<true, INV_FULL, LB>(log_n, P, npolys, g == 2, st);
+    if (s != NTTB_DECLINED) return s;
   }
   if (use_passes(log_n, npolys, true)) {
     const int LAT_LOG_R = lat_log_r(log_n);
