@@ -589,13 +589,18 @@ def modmul_roof(nt, basis, stream):
                 ctypes.byref(cnt), stream.cuda_stream)
         nt._lib.call("nttmul_modmul_roof", *args)  # warm
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(5):
-            nt._lib.call("nttmul_modmul_roof", *args)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        best[label] = 5 * cnt.value / (e0.elapsed_time(e1) / 1e3) / 1e9
+        # best of 3 timed groups: a roof is the fastest rate the loop
+        # reaches (one group alone read up to 3 % low on a clock ramp, r2)
+        rates = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(5):
+                nt._lib.call("nttmul_modmul_roof", *args)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            rates.append(5 * cnt.value / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        best[label] = max(rates)
     # int-pipe roof: the fastest register-resident rate of any modmul form
     # (bare Shoup product, Barrett product, lazy CT / GS butterfly = one
     # modmul plus its add/sub/correction), no memory traffic at all

@@ -92,8 +92,14 @@ enum InvKind { INV_NONE = 0, INV_FULL = 1, INV_SKIP = 2 };
 #define NTTB_ROW_TAIL_G 1  // standalone rows: tail reads / writes global directly
 #endif
 
-template <int LOG_R, int LOG_E = NTTB_ROW_LOG_E>
+#ifndef NTTB_ROW_LOG_E12
+#define NTTB_ROW_LOG_E12 NTTB_ROW_LOG_E  // elements per thread of the 4096-word rows
+#endif
+constexpr int row_log_e(int log_r) { return log_r == 12 ? NTTB_ROW_LOG_E12 : NTTB_ROW_LOG_E; }
+
+template <int LOG_R, int LOG_E = row_log_e(LOG_R)>
 struct RowGeom {
+  static constexpr int LE = LOG_E;
   static constexpr int N2 = 1 << LOG_R;
   static constexpr int E = 1 << LOG_E;
   static constexpr int T = N2 / E;                 // threads per CTA
@@ -275,8 +281,8 @@ __device__ __forceinline__ void head_inv(u64 *__restrict__ sm,
 template <int LOG_R, int S0_BLOCK>
 __device__ __forceinline__ void row_sync() {
   using G = RowGeom<LOG_R>;
-  constexpr bool ONE_UNIT = G::HEAD % G::NPASS == 0 && G::HEAD / G::NPASS == NTTB_ROW_LOG_E;
-  constexpr int THREADS = 1 << (LOG_R - S0_BLOCK - NTTB_ROW_LOG_E);
+  constexpr bool ONE_UNIT = G::HEAD % G::NPASS == 0 && G::HEAD / G::NPASS == G::LE;
+  constexpr int THREADS = 1 << (LOG_R - S0_BLOCK - G::LE);
   if constexpr (!NTTB_LOCAL_SYNC || !ONE_UNIT || THREADS >= G::T) {
     __syncthreads();
   } else if constexpr (THREADS <= 32) {
@@ -544,7 +550,7 @@ __global__ void __launch_bounds__(RowGeom<LOG_R>::T, (row_minb<LOG_R, MID>()))
 
   __shared__ u64 sbar[2];  // a's / b's first pass written
   if constexpr (MID) {
-    static_assert(G::R(0) == NTTB_ROW_LOG_E && G::NPASS >= 2, "fused row geometry");
+    static_assert(G::R(0) == G::LE && G::NPASS >= 2, "fused row geometry");
     // b's row streams into its smem slot (cp.async, each thread exactly the
     // words its own first-pass unit reads) while a's first pass loads and
     // transforms a.  The CTA-wide dependency pass 0 -> pass 1 is split per
