@@ -563,10 +563,11 @@ def test_verify_suites_pass():
     assert "polymul-three-way x100" in names and "rns-roundtrip x20" in names
 
 
-@pytest.mark.parametrize("log_n,limbs,batch", [(14, 8, 64), (17, 32, 8)])
+@pytest.mark.parametrize("log_n,limbs,batch", [(14, 8, 64), (16, 21, 64), (17, 32, 8)])
 def test_baseline_configs_full_batch(log_n, limbs, batch):
-    """BASELINE cfg2 (N=2^14, 8 limbs, 64 products) and cfg4 (N=2^17, 32
-    limbs, 8 ciphertexts) at full size: first and last ciphertext against the
+    """BASELINE cfg2 (N=2^14, 8 limbs, 64 products), cfg3 at bench.py's
+    default batch (N=2^16, 21 limbs, 64 ciphertexts = the two-stream split)
+    and cfg4 (N=2^17, 32 limbs, 8 ciphertexts) at full size: first and last ciphertext against the
     oracle, and bilinearity c(a, b1 + b2) = c(a, b1) + c(a, b2) mod q over the
     whole batch (a size-independent check of every product)."""
     basis = nt.RnsBasis.build(1 << log_n, 60, limbs, seed=0)
