@@ -480,6 +480,8 @@ def main():
     row_ms = phase_ms["row_fused"]
     row_rate = products_per_step * row_kernel_modmuls(n) / (row_ms / 1e3) / 1e9
     all_rate = products_per_step * modmuls_per_product(n) / (ms / args.steps / 1e3) / 1e9
+    if share and world > 1:  # the ranks' steps ran concurrently on the one GPU
+        all_rate = world * products_per_step * modmuls_per_product(n) / (ms_per_step / 1e3) / 1e9
     traffic = load_traffic(products_per_step, n)
     pipe = imad_pipe_roof(n, clk.summary().get("sm_mhz"))
     roofline = {
