@@ -651,6 +651,9 @@ def load_traffic(products: int, n: int):
         return None
     kernels = ("col_fwd", "row_fused", "col_inv") if n > 4096 else ("row_fused",)
     out = {}
+    by_n = rec.get("by_n", {}).get(str(n))  # per-size captures (cfg2 / cfg4)
+    if by_n:
+        rec = {**by_n, "source": by_n.get("source", rec.get("source"))}
     for k in kernels:
         r = rec.get(k)
         if r and r.get("n", n) == n:
